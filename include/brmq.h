@@ -1,0 +1,182 @@
+/*
+ * brmq.h -- C-ABI of the B200-native batched range-minimum-query engine
+ * (arXiv 1706.06940, BbST / BbST_CON) -- the drop-in boundary.
+ *
+ * The reference exposes C++ free functions in namespace `batchrmq`
+ * (/root/reference/proj/core/include/batchrmq/*.hpp) plus the SPEC-level
+ * solves.  Each entry point below replaces one of
+ * them; the cited file:line is the interface it stands in for.  Plain
+ * pointers and sizes only; no C++ or torch types cross this boundary.
+ *
+ * Semantics shared by every entry point:
+ *   - Positions are 0-based, queries inclusive [left, right]; a query with
+ *     left > right is normalised by swapping, exactly as the
+ *     batchrmq::Query constructor does (types.hpp:18-20).
+ *   - Every answer is the LEFTMOST position of the minimum of A[left..right],
+ *     bit-identical to naive_rmq (naive.hpp:13-21).  Answers are emitted in
+ *     input order (types.hpp:25-29).
+ *   - Errors are status codes that map 1:1 onto the reference's exception
+ *     classes (BRMQ_EDOMAIN = std::domain_error, ...); brmq_last_error()
+ *     returns the thread-local message.  include/batchrmq_cuda.hpp rethrows
+ *     them as the same std:: types.
+ *   - A context owns one CUDA stream and a grow-only device workspace.  One
+ *     context must not be used by two threads at once; distinct contexts may
+ *     run concurrently.
+ *   - BRMQ_PTR_DEVICE in `flags` says A / Q / answers are device pointers
+ *     (resident in HBM); otherwise they are host pointers and the call copies
+ *     them in and out on the context stream.  Every call returns after the
+ *     answers are complete (host or device).
+ *
+ * The only limits are the reference's: n <= 2^32 - 1 (32-bit positions,
+ * element_sparse_table.cpp:12-13, contraction.hpp:13) and q <= 2^31
+ * (contraction.cpp:14-15).
+ */
+#ifndef BRMQ_H
+#define BRMQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* == batchrmq::Query (types.hpp:13-23): 16 B, left @0, right @8. */
+typedef struct brmq_query {
+    uint64_t left;
+    uint64_t right;
+} brmq_query;
+
+/* == batchrmq::Endpoint (contraction.hpp:12-21): origin = (qi << 1) | is_right. */
+typedef struct brmq_endpoint {
+    uint32_t pos;
+    uint32_t origin;
+} brmq_endpoint;
+
+typedef struct brmq_ctx brmq_ctx;
+
+enum brmq_status {
+    BRMQ_OK = 0,
+    BRMQ_EDOMAIN = 1, /* std::domain_error    (bits.hpp:11)                          */
+    BRMQ_ERANGE = 2,  /* std::out_of_range    (naive.hpp:15, element_sparse_table.cpp:37) */
+    BRMQ_EINVAL = 3,  /* std::invalid_argument (contraction.cpp:15,123; est.cpp:11,13,36) */
+    BRMQ_ELOGIC = 4,  /* std::logic_error     (contraction.cpp:159,183)                */
+    BRMQ_ECUDA = 5,   /* CUDA runtime failure (no reference equivalent)               */
+    BRMQ_ENOMEM = 6   /* std::bad_alloc / cudaErrorMemoryAllocation                   */
+};
+
+enum brmq_flags {
+    BRMQ_PTR_HOST = 0,
+    BRMQ_PTR_DEVICE = 1 /* A, Q, answers (and stage buffers) are device pointers */
+};
+
+enum brmq_sort_kind { /* == batchrmq::SortKind (contraction.hpp:23) */
+    BRMQ_SORT_RADIX = 0,
+    BRMQ_SORT_COMPARISON = 1
+};
+
+/* ------------------------------------------------------------ context */
+int brmq_ctx_create(brmq_ctx** out, int device);
+void brmq_ctx_destroy(brmq_ctx* ctx);
+/* Use a caller-owned cudaStream_t (NULL restores the context's own stream). */
+int brmq_ctx_set_stream(brmq_ctx* ctx, void* cuda_stream);
+void* brmq_ctx_stream(brmq_ctx* ctx);
+/* Thread-local message of the last failing call on this thread. */
+const char* brmq_last_error(void);
+
+/* ------------------------------------------------------------- solves */
+
+/* SPEC.md:302-310 solve_batch_bbst(array, batch, LevelConfig{[k]}) -- BbST with
+ * no contraction: block-argmin scan over A, block Sparse
+ * Table over the n/k block minima, speculative query answering. */
+int brmq_solve_bbst(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
+                    uint64_t q, uint32_t k, uint64_t* answers, uint32_t flags);
+
+/* SPEC.md:237-245 solve_batch_bbst_con(array, batch, BbstConParams{k, sort_kind})
+ * -- BbST_CON: endpoint sort, contraction of A into A_Q,
+ * block Sparse Table over A_Q, speculative answering. */
+int brmq_solve_bbst_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
+                        uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
+                        uint32_t flags);
+
+/* ------------------------------------------------ stage-level entry points */
+
+/* contraction.hpp:51 collect_endpoints (contraction.cpp:13-23): eps gets 2q
+ * endpoints in collect order (left, right per query). */
+int brmq_collect_endpoints(brmq_ctx* ctx, const brmq_query* Q, uint64_t q, brmq_endpoint* eps,
+                           uint32_t flags);
+
+/* contraction.hpp:55 sort_endpoints (contraction.cpp:27-74): in place, by pos,
+ * non-decreasing.  The device sort is a stable LSD radix sort for both kinds,
+ * so the order equals the reference Radix sort's exactly. */
+int brmq_sort_endpoints(brmq_ctx* ctx, brmq_endpoint* eps, uint64_t m, int sort_kind,
+                        uint32_t flags);
+
+/* contraction.hpp:61-64 build_contracted (contraction.cpp:112-151): boundary
+ * (>= m entries) gets the deduplicated sorted positions, *nb their count;
+ * aq_values / aq_origin (>= m entries) get the nb-1 inclusive area minima and
+ * their leftmost positions. */
+int brmq_build_contracted(brmq_ctx* ctx, const int32_t* A, uint64_t n,
+                          const brmq_endpoint* sorted_eps, uint64_t m, int32_t* aq_values,
+                          uint64_t* aq_origin, uint64_t* boundary, uint64_t* nb,
+                          uint32_t flags);
+
+/* contraction.hpp:71-73 remap_queries_from_sorted (contraction.cpp:174-199). */
+int brmq_remap_from_sorted(brmq_ctx* ctx, const brmq_endpoint* sorted_eps, uint64_t m,
+                           const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cleft,
+                           uint32_t* cright, uint8_t* degenerate, uint32_t flags);
+
+/* SPEC.md:210-218 build_block_sparse(values, k): table[e*b + j] (b = ceil(m/k),
+ * levels = floor_log2(b)+1, table sized levels*b) = position of the leftmost
+ * minimum over blocks j .. j+2^e-1; cells whose span does not fit are
+ * UINT64_MAX.  *b_out / *levels_out receive b and levels. */
+int brmq_build_block_sparse(brmq_ctx* ctx, const int32_t* values, uint64_t m, uint32_t k,
+                            uint64_t* table, uint64_t* b_out, uint32_t* levels_out,
+                            uint32_t flags);
+
+/* bits.hpp:10-13 floor_log2 (host; BRMQ_EDOMAIN on 0). */
+int brmq_floor_log2(uint64_t x, uint32_t* out);
+
+/* --------------------------------------------------------- instrumentation */
+
+/* Per-stage device times of the last solve on this context, measured with
+ * CUDA events on the context stream (only while timing is enabled; events
+ * are recorded around every kernel launch and add no synchronisation). */
+#define BRMQ_MAX_STAGES 16
+typedef struct brmq_stage_times {
+    int count;
+    char name[BRMQ_MAX_STAGES][24];
+    float ms[BRMQ_MAX_STAGES];
+    uint32_t launches[BRMQ_MAX_STAGES]; /* kernel launches inside the stage */
+} brmq_stage_times;
+
+int brmq_ctx_set_timing(brmq_ctx* ctx, int enable);
+int brmq_last_stage_times(brmq_ctx* ctx, brmq_stage_times* out);
+
+/* Facts about the last solve: sizes of the intermediate structures and the
+ * number of kernel launches it issued. */
+typedef struct brmq_solve_info {
+    uint64_t n, q, k;
+    uint64_t blocks;        /* b = ceil(len/k) of the block Sparse Table   */
+    uint32_t levels;        /* floor_log2(b) + 1                          */
+    uint64_t boundary;      /* contraction: |boundary| (0 for BbST)       */
+    uint64_t span_lo;       /* contraction: boundary[0]                   */
+    uint64_t span_hi;       /* contraction: boundary[last]                */
+    uint32_t kernel_launches;
+} brmq_solve_info;
+
+int brmq_last_solve_info(brmq_ctx* ctx, brmq_solve_info* out);
+
+/* Host pinned memory helpers (cudaHostAlloc / cudaFreeHost) so callers can
+ * keep H2D/D2H at full PCIe rate without linking the CUDA runtime. */
+int brmq_host_alloc(void** out, size_t bytes);
+int brmq_host_free(void* p);
+int brmq_device_alloc(brmq_ctx* ctx, void** out, size_t bytes);
+int brmq_device_free(brmq_ctx* ctx, void* p);
+int brmq_memcpy(brmq_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* cudaMemcpyKind */);
+int brmq_synchronize(brmq_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BRMQ_H */

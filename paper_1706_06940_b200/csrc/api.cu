@@ -1,0 +1,722 @@
+// api.cu -- the C-ABI (include/brmq.h): context, workspace, validation and the
+// stream-ordered orchestration of the sm_100a kernels.
+//
+// Each extern "C" entry point stands in for one reference function (see
+// brmq.h for the file:line map).  The host code never computes an answer: if
+// the device path cannot run the call fails with BRMQ_ECUDA -- there is no CPU
+// fallback anywhere in this library.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/brmq.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? BRMQ_ENOMEM : BRMQ_ECUDA,        \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+// Control block of one call: zeroed by one memset at the start of every solve.
+struct Control {
+    uint32_t err;       // 1 query out of range (direct), 2 range (collect/unique), 4 unsorted, 8 logic
+    uint32_t span[2];   // [~min endpoint, max endpoint]
+    uint32_t tickets[5];
+    uint64_t nb;        // |boundary|
+    uint64_t aq_len;    // |A_Q|
+    uint64_t b_dev;     // blocks over A_Q
+};
+
+}  // namespace
+
+struct brmq_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    char* ws = nullptr;  // grow-only workspace (zeroed on growth)
+    size_t ws_cap = 0;
+    uint32_t* bitmap = nullptr;  // persistent, kept all-zero by the contraction kernel
+    size_t bitmap_words = 0;
+    Control* ctl_host = nullptr;  // pinned mirror of the control block
+    uint32_t epoch = 1;
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::string> stage_names;
+    std::vector<uint32_t> stage_launches;
+    brmq_stage_times last_times{};
+    brmq_solve_info info{};
+};
+
+namespace {
+
+// Bump allocator over the context workspace; call plan() for every buffer,
+// then commit() (grows the workspace if needed), then get pointers by index.
+struct Carve {
+    std::vector<size_t> off;
+    size_t total = 0;
+    size_t add(size_t bytes) {
+        off.push_back(total);
+        total += align_up(bytes ? bytes : 1);
+        return off.size() - 1;
+    }
+};
+
+int ensure_ws(brmq_ctx* c, size_t bytes) {
+    if (bytes <= c->ws_cap) return BRMQ_OK;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->ws) cudaFree(c->ws);
+    c->ws = nullptr;
+    c->ws_cap = 0;
+    size_t cap = align_up(bytes + bytes / 8, 1 << 21);
+    CUDA_TRY(cudaMalloc(&c->ws, cap));
+    CUDA_TRY(cudaMemsetAsync(c->ws, 0, cap, c->stream));  // status words start invalid
+    c->ws_cap = cap;
+    return BRMQ_OK;
+}
+
+int ensure_bitmap(brmq_ctx* c, uint64_t n) {
+    const size_t words = size_t(n / 32 + 2);
+    if (words <= c->bitmap_words) return BRMQ_OK;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->bitmap) cudaFree(c->bitmap);
+    c->bitmap = nullptr;
+    c->bitmap_words = 0;
+    CUDA_TRY(cudaMalloc(&c->bitmap, words * 4));
+    CUDA_TRY(cudaMemsetAsync(c->bitmap, 0, words * 4, c->stream));
+    c->bitmap_words = words;
+    return BRMQ_OK;
+}
+
+// Reserve `count` consecutive 24-bit epochs for single-pass scans.
+uint32_t take_epochs(brmq_ctx* c, uint32_t count) {
+    if (c->epoch + count >= (1u << 24)) {
+        // wrap: every status word in the workspace is reset to "invalid"
+        cudaMemsetAsync(c->ws, 0, c->ws_cap, c->stream);
+        c->epoch = 1;
+    }
+    const uint32_t e = c->epoch;
+    c->epoch += count;
+    return e;
+}
+
+// ------------------------------------------------------------------ timing
+struct Timer {
+    brmq_ctx* c;
+    int n = 0;
+    explicit Timer(brmq_ctx* ctx) : c(ctx) {
+        c->stage_names.clear();
+        c->stage_launches.clear();
+    }
+    void stage(const char* name, int launches_before) {
+        (void)launches_before;
+        if (!c->timing || n >= BRMQ_MAX_STAGES) return;
+        cudaEventRecord(c->ev[2 * n], c->stream);
+        c->stage_names.emplace_back(name);
+        c->stage_launches.push_back(0);
+    }
+    void end(int launches) {
+        if (!c->timing || n >= BRMQ_MAX_STAGES) return;
+        cudaEventRecord(c->ev[2 * n + 1], c->stream);
+        c->stage_launches.back() = uint32_t(launches);
+        ++n;
+    }
+    void finish() {
+        brmq_stage_times& t = c->last_times;
+        std::memset(&t, 0, sizeof(t));
+        if (!c->timing) return;
+        t.count = n;
+        for (int i = 0; i < n; ++i) {
+            std::snprintf(t.name[i], sizeof(t.name[i]), "%s", c->stage_names[i].c_str());
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]);
+            t.ms[i] = ms;
+            t.launches[i] = c->stage_launches[i];
+        }
+    }
+};
+
+bool is_device(uint32_t flags) { return (flags & BRMQ_PTR_DEVICE) != 0; }
+
+int check_status(brmq_ctx* c) {
+    CUDA_TRY(cudaGetLastError());
+    return BRMQ_OK;
+}
+
+int sync_and_read_control(brmq_ctx* c, const Control* ctl_dev) {
+    CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl_dev, sizeof(Control), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return BRMQ_OK;
+}
+
+int map_err(uint32_t err) {
+    if (err & 8u) return fail(BRMQ_ELOGIC, "remap_queries_from_sorted: endpoint missing from boundary");
+    if (err & 4u) return fail(BRMQ_EINVAL, "build_contracted: endpoints not sorted");
+    if (err & 3u) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    return BRMQ_OK;
+}
+
+int bits_for(uint64_t n) {  // bit_width(n - 1): positions are < n
+    if (n <= 1) return 0;
+    return 64 - __builtin_clzll(n - 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* brmq_last_error(void) { return g_last_error.c_str(); }
+
+int brmq_floor_log2(uint64_t x, uint32_t* out) {
+    if (x == 0) return fail(BRMQ_EDOMAIN, "floor_log2: argument must be positive");  // bits.hpp:11
+    *out = 63u - uint32_t(__builtin_clzll(x));
+    return BRMQ_OK;
+}
+
+int brmq_ctx_create(brmq_ctx** out, int device) {
+    if (!out) return fail(BRMQ_EINVAL, "brmq_ctx_create: null out");
+    *out = nullptr;
+    int count = 0;
+    CUDA_TRY(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(BRMQ_EINVAL, "brmq_ctx_create: no device %d", device);
+    CUDA_TRY(cudaSetDevice(device));
+    auto* c = new brmq_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(BRMQ_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    c->stream = c->own;
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->ctl_host), sizeof(Control), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(c->own);
+        delete c;
+        return fail(BRMQ_ECUDA, "cudaHostAlloc: %s", cudaGetErrorString(e));
+    }
+    c->ev.resize(2 * BRMQ_MAX_STAGES);
+    for (auto& x : c->ev) cudaEventCreate(&x);
+    *out = c;
+    return BRMQ_OK;
+}
+
+void brmq_ctx_destroy(brmq_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& x : c->ev) cudaEventDestroy(x);
+    if (c->ws) cudaFree(c->ws);
+    if (c->bitmap) cudaFree(c->bitmap);
+    if (c->ctl_host) cudaFreeHost(c->ctl_host);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+}
+
+int brmq_ctx_set_stream(brmq_ctx* c, void* s) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+    return BRMQ_OK;
+}
+
+void* brmq_ctx_stream(brmq_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int brmq_ctx_set_timing(brmq_ctx* c, int enable) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    c->timing = enable != 0;
+    return BRMQ_OK;
+}
+
+int brmq_last_stage_times(brmq_ctx* c, brmq_stage_times* out) {
+    if (!c || !out) return fail(BRMQ_EINVAL, "null argument");
+    *out = c->last_times;
+    return BRMQ_OK;
+}
+
+int brmq_last_solve_info(brmq_ctx* c, brmq_solve_info* out) {
+    if (!c || !out) return fail(BRMQ_EINVAL, "null argument");
+    *out = c->info;
+    return BRMQ_OK;
+}
+
+int brmq_host_alloc(void** out, size_t bytes) {
+    CUDA_TRY(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault));
+    return BRMQ_OK;
+}
+int brmq_host_free(void* p) {
+    CUDA_TRY(cudaFreeHost(p));
+    return BRMQ_OK;
+}
+int brmq_device_alloc(brmq_ctx* c, void** out, size_t bytes) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMalloc(out, bytes ? bytes : 1));
+    return BRMQ_OK;
+}
+int brmq_device_free(brmq_ctx* c, void* p) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaFree(p));
+    return BRMQ_OK;
+}
+int brmq_memcpy(brmq_ctx* c, void* dst, const void* src, size_t bytes, int kind) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyKind(kind), c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return BRMQ_OK;
+}
+int brmq_synchronize(brmq_ctx* c) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return BRMQ_OK;
+}
+
+// ------------------------------------------------------------------ BbST (h = 1)
+int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
+                    uint32_t k, uint64_t* answers, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    c->info.k = k;
+    Timer tm(c);
+    if (q == 0) {  // SPEC.md:306 empty batch -> empty answers
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t b = (n + k - 1) / k;
+    const uint32_t L = brmq::floor_log2_u64(b) + 1;
+
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_st = cv.add(size_t(L) * b * 8);
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    int launches = 0;
+
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    if (!dev) {
+        tm.stage("h2d", launches);
+        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+        tm.end(0);
+    }
+    tm.stage("block_argmin", launches);
+    int l = brmq::launch_block_argmin_i32(dA, n, k, ST, s);
+    launches += l;
+    tm.end(l);
+    tm.stage("sparse_table", launches);
+    l = brmq::launch_sparse_table(ST, b, nullptr, s);
+    launches += l;
+    tm.end(l);
+    tm.stage("query", launches);
+    l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s);
+    launches += l;
+    tm.end(l);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) {
+        tm.stage("d2h", launches);
+        CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+        tm.end(0);
+    }
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    tm.finish();
+    c->info.blocks = b;
+    c->info.levels = L;
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(c->ctl_host->err);
+}
+
+// ------------------------------------------------------------------ BbST_CON
+int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q,
+                        uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
+                        uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst_con: block size k must be >= 1");
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
+    if (sort_kind < 0 || sort_kind > 2) return fail(BRMQ_EINVAL, "unknown sort kind %d", sort_kind);
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    c->info.k = k;
+    Timer tm(c);
+    if (q == 0) {
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const bool use_bitmap = sort_kind == 2;
+    const uint64_t m = 2 * q;
+    const uint64_t aq_max = m - 1;                       // |A_Q| <= 2q - 1
+    const uint64_t b_max = (aq_max + k - 1) / k;
+    const uint32_t L = brmq::floor_log2_u64(b_max) + 1;
+    const uint64_t ntiles = brmq::contract_tiles(n);
+    const int bits = bits_for(n);
+    if (int rc = ensure_bitmap(c, n)) return rc;
+
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_cl = cv.add(q * 4);
+    const size_t i_cr = cv.add(q * 4);
+    const size_t i_aq = cv.add((aq_max + 2) * 8);
+    const size_t i_st = cv.add(size_t(L) * b_max * 8);
+    const size_t i_cst = cv.add(ntiles * 8);
+    const size_t i_kag = cv.add(ntiles * 8);
+    const size_t i_kin = cv.add(ntiles * 8);
+    size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_ust = 0, i_wi = 0;
+    if (use_bitmap) {
+        i_wi = cv.add((n / 32 + 2) * 8);
+    } else {
+        i_k0 = cv.add(m * 4);
+        i_v0 = cv.add(m * 4);
+        i_k1 = cv.add(m * 4);
+        i_v1 = cv.add(m * 4);
+        i_rs = cv.add(brmq::radix_sort_temp_bytes(m, bits));
+        i_ust = cv.add(brmq::unique_status_words(m) * 8);
+    }
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    auto* cl = reinterpret_cast<uint32_t*>(P(i_cl));
+    auto* cr = reinterpret_cast<uint32_t*>(P(i_cr));
+    auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
+    auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
+    auto* cst = reinterpret_cast<uint64_t*>(P(i_cst));
+    auto* kag = reinterpret_cast<uint64_t*>(P(i_kag));
+    auto* kin = reinterpret_cast<uint64_t*>(P(i_kin));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    int launches = 0, l = 0;
+
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    if (!dev) {
+        tm.stage("h2d", launches);
+        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+        tm.end(0);
+    }
+    const uint32_t ep_contract = take_epochs(c, 1);
+    if (use_bitmap) {
+        tm.stage("collect_mark", launches);
+        l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->span, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+    } else {
+        auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
+        auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
+        auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
+        auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
+        tm.stage("collect", launches);
+        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("radix_sort", launches);
+        bool in_alt = false;
+        const uint32_t ep = take_epochs(c, uint32_t(brmq::radix_sort_passes(bits)));
+        l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), s, &in_alt, ep);
+        launches += l;
+        tm.end(l);
+        tm.stage("unique_rank", launches);
+        const uint32_t ep_u = take_epochs(c, 1);
+        l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr, c->bitmap,
+                                ctl->span, &ctl->nb, &ctl->err,
+                                reinterpret_cast<uint64_t*>(P(i_ust)), &ctl->tickets[0], ep_u, s);
+        launches += l;
+        tm.end(l);
+    }
+    tm.stage("contract", launches);
+    l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, cst, kag, kin, &ctl->tickets[1],
+                              ep_contract, AQ, &ctl->aq_len, &ctl->nb,
+                              use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, s);
+    launches += l;
+    tm.end(l);
+    if (use_bitmap) {
+        tm.stage("remap", launches);
+        l = brmq::launch_remap_bitmap(dQ, q, n, reinterpret_cast<uint2*>(P(i_wi)), cl, cr, s);
+        launches += l;
+        tm.end(l);
+    }
+    tm.stage("block_argmin", launches);
+    l = brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
+    launches += l;
+    tm.end(l);
+    tm.stage("sparse_table", launches);
+    l = brmq::launch_sparse_table(ST, b_max, &ctl->b_dev, s);
+    launches += l;
+    tm.end(l);
+    tm.stage("query", launches);
+    l = brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr, q, dAns, s);
+    launches += l;
+    tm.end(l);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) {
+        tm.stage("d2h", launches);
+        CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+        tm.end(0);
+    }
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    tm.finish();
+    const Control& h = *c->ctl_host;
+    c->info.boundary = h.nb;
+    c->info.span_lo = ~h.span[0];
+    c->info.span_hi = h.span[1];
+    c->info.blocks = h.b_dev;
+    c->info.levels = h.b_dev ? brmq::floor_log2_u64(h.b_dev) + 1 : 0;
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(h.err);
+}
+
+// ------------------------------------------------------------ stage entry points
+int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_endpoint* eps,
+                           uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
+    if (q == 0) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t m = 2 * q;
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_k = cv.add(m * 4), i_v = cv.add(m * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_e = dev ? 0 : cv.add(m * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+    auto* k = reinterpret_cast<uint32_t*>(P(i_k));
+    auto* v = reinterpret_cast<uint32_t*>(P(i_v));
+    brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
+    brmq::launch_join_eps(k, v, m, dE, s);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return BRMQ_OK;
+}
+
+int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_kind, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (sort_kind < 0 || sort_kind > 2) return fail(BRMQ_EINVAL, "unknown sort kind %d", sort_kind);
+    if (m < 2) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    Carve cv;
+    const size_t i_k0 = cv.add(m * 4), i_v0 = cv.add(m * 4), i_k1 = cv.add(m * 4), i_v1 = cv.add(m * 4);
+    const size_t i_rs = cv.add(brmq::radix_sort_temp_bytes(m, 32));
+    const size_t i_e = dev ? 0 : cv.add(m * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(dE, eps, m * 8, cudaMemcpyHostToDevice, s));
+    auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
+    auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
+    auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
+    auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
+    brmq::launch_split_eps(dE, m, k0, v0, s);
+    bool in_alt = false;
+    const uint32_t ep = take_epochs(c, 4);
+    brmq::launch_radix_sort(k0, v0, k1, v1, m, 32, P(i_rs), s, &in_alt, ep);
+    brmq::launch_join_eps(in_alt ? k1 : k0, in_alt ? v1 : v0, m, dE, s);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return BRMQ_OK;
+}
+
+int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_endpoint* sorted_eps,
+                          uint64_t m, int32_t* aq_values, uint64_t* aq_origin, uint64_t* boundary,
+                          uint64_t* nb, uint32_t flags) {
+    if (!c || !nb) return fail(BRMQ_EINVAL, "null argument");
+    *nb = 0;
+    if (m == 0) return BRMQ_OK;  // contraction.cpp:116
+    if (n == 0) return fail(BRMQ_ERANGE, "endpoint exceeds array bounds");
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    if (int rc = ensure_bitmap(c, n)) return rc;
+    const uint64_t ntiles = brmq::contract_tiles(n);
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_k = cv.add(m * 4), i_v = cv.add(m * 4), i_bd = cv.add(m * 4);
+    const size_t i_aq = cv.add((m + 2) * 8);
+    const size_t i_ust = cv.add(brmq::unique_status_words(m) * 8);
+    const size_t i_cst = cv.add(ntiles * 8), i_kag = cv.add(ntiles * 8), i_kin = cv.add(ntiles * 8);
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_e = dev ? 0 : cv.add(m * 8);
+    const size_t i_av = dev ? 0 : cv.add(m * 4);
+    const size_t i_ao = dev ? 0 : cv.add(m * 8);
+    const size_t i_bo = dev ? 0 : cv.add(m * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const void* dE = dev ? static_cast<const void*>(sorted_eps) : static_cast<void*>(P(i_e));
+    int32_t* dav = dev ? aq_values : reinterpret_cast<int32_t*>(P(i_av));
+    uint64_t* dao = dev ? aq_origin : reinterpret_cast<uint64_t*>(P(i_ao));
+    uint64_t* dbo = dev ? boundary : reinterpret_cast<uint64_t*>(P(i_bo));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    if (!dev) {
+        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
+    }
+    auto* k = reinterpret_cast<uint32_t*>(P(i_k));
+    auto* v = reinterpret_cast<uint32_t*>(P(i_v));
+    auto* bd = reinterpret_cast<uint32_t*>(P(i_bd));
+    auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
+    brmq::launch_split_eps(dE, m, k, v, s);
+    const uint32_t ep_u = take_epochs(c, 1), ep_c = take_epochs(c, 1);
+    brmq::launch_unique(k, v, m, n, bd, nullptr, nullptr, c->bitmap, ctl->span, &ctl->nb, &ctl->err,
+                        reinterpret_cast<uint64_t*>(P(i_ust)), &ctl->tickets[0], ep_u, s);
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    if (c->ctl_host->err) {
+        // unsorted or out-of-range endpoints: clear any marks and report
+        CUDA_TRY(cudaMemsetAsync(c->bitmap, 0, c->bitmap_words * 4, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return map_err(c->ctl_host->err);
+    }
+    brmq::launch_contract(dA, n, c->bitmap, ctl->span, reinterpret_cast<uint64_t*>(P(i_cst)),
+                          reinterpret_cast<uint64_t*>(P(i_kag)), reinterpret_cast<uint64_t*>(P(i_kin)),
+                          &ctl->tickets[1], ep_c, AQ, &ctl->aq_len, &ctl->nb, nullptr, s);
+    brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);
+    brmq::launch_u32_to_u64(bd, &ctl->nb, m, dbo, s);
+    if (int rc = check_status(c)) return rc;
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    const uint64_t nbv = c->ctl_host->nb;
+    const uint64_t areas = nbv > 0 ? nbv - 1 : 0;
+    if (!dev) {
+        if (areas) {
+            CUDA_TRY(cudaMemcpyAsync(aq_values, dav, areas * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(aq_origin, dao, areas * 8, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_TRY(cudaMemcpyAsync(boundary, dbo, nbv * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    *nb = nbv;
+    return map_err(c->ctl_host->err);
+}
+
+int brmq_remap_from_sorted(brmq_ctx* c, const brmq_endpoint* sorted_eps, uint64_t m,
+                           const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cleft,
+                           uint32_t* cright, uint8_t* degenerate, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (q == 0 && m == 0) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_k = cv.add(m * 4), i_v = cv.add(m * 4);
+    const size_t i_e = dev ? 0 : cv.add(m * 8);
+    const size_t i_b = dev ? 0 : cv.add(nb * 8);
+    const size_t i_cl = dev ? 0 : cv.add(q * 4), i_cr = dev ? 0 : cv.add(q * 4);
+    const size_t i_dg = dev ? 0 : cv.add(q);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    const void* dE = dev ? static_cast<const void*>(sorted_eps) : static_cast<void*>(P(i_e));
+    const uint64_t* dB = dev ? boundary : reinterpret_cast<uint64_t*>(P(i_b));
+    uint32_t* dcl = dev ? cleft : reinterpret_cast<uint32_t*>(P(i_cl));
+    uint32_t* dcr = dev ? cright : reinterpret_cast<uint32_t*>(P(i_cr));
+    uint8_t* ddg = dev ? degenerate : reinterpret_cast<uint8_t*>(P(i_dg));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    if (!dev) {
+        if (m) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
+        if (nb) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dB), boundary, nb * 8, cudaMemcpyHostToDevice, s));
+    }
+    if (q) {
+        CUDA_TRY(cudaMemsetAsync(dcl, 0, q * 4, s));
+        CUDA_TRY(cudaMemsetAsync(dcr, 0, q * 4, s));
+    }
+    auto* k = reinterpret_cast<uint32_t*>(P(i_k));
+    auto* v = reinterpret_cast<uint32_t*>(P(i_v));
+    brmq::launch_split_eps(dE, m, k, v, s);
+    brmq::launch_remap_search(k, v, m, dB, nb, q, dcl, dcr, ddg, &ctl->err, s);
+    if (int rc = check_status(c)) return rc;
+    if (!dev && q) {
+        CUDA_TRY(cudaMemcpyAsync(cleft, dcl, q * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(cright, dcr, q * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(degenerate, ddg, q, cudaMemcpyDeviceToHost, s));
+    }
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    return map_err(c->ctl_host->err);
+}
+
+int brmq_build_block_sparse(brmq_ctx* c, const int32_t* values, uint64_t m, uint32_t k,
+                            uint64_t* table, uint64_t* b_out, uint32_t* levels_out, uint32_t flags) {
+    if (!c || !b_out || !levels_out) return fail(BRMQ_EINVAL, "null argument");
+    if (k == 0) return fail(BRMQ_EINVAL, "build_block_sparse: k must be >= 1");
+    if (m > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    const uint64_t b = (m + k - 1) / k;
+    *b_out = b;
+    *levels_out = b ? brmq::floor_log2_u64(b) + 1 : 0;
+    if (b == 0) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t cells = uint64_t(*levels_out) * b;
+    Carve cv;
+    const size_t i_v = dev ? 0 : cv.add(m * 4);
+    const size_t i_t = dev ? 0 : cv.add(cells * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    const int32_t* dV = dev ? values : reinterpret_cast<int32_t*>(P(i_v));
+    uint64_t* dT = dev ? table : reinterpret_cast<uint64_t*>(P(i_t));
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dV), values, m * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(dT, 0xFF, cells * 8, s));
+    brmq::launch_block_argmin_i32(dV, m, k, dT, s);
+    brmq::launch_sparse_table(dT, b, nullptr, s);
+    brmq::launch_keys_to_pos(dT, cells, s);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) CUDA_TRY(cudaMemcpyAsync(table, dT, cells * 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return BRMQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+// block_argmin.cu -- level 0 of the block Sparse Table (K1).
+//
+// SPEC.md:199-203 / :213 / :253: level-0 entry j is the leftmost-minimum
+// position of block B_j = [j*k, min((j+1)*k, m)); the trailing partial block
+// is clipped (no +inf padding).  PAPER.md:304-309 (BbST stage 1).
+//
+// B200 design: this is one streaming pass over A (4n bytes, HBM-bound).
+// One warp owns one block: each lane issues 128-bit non-allocating loads
+// (ld.global.nc.L1::no_allocate.v4), 4 vectors per lane in flight per round,
+// keeps its leftmost minimum in registers, and the warp combines lanes with
+// two redux.sync (value, then leftmost position) -- no shared memory, no
+// block barrier.  Output is one packed key per block (8 B).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace brmq {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnroll = 4;  // 16-byte vectors per lane in flight
+
+// k % 128 == 0, A 16-byte aligned: full blocks [0, nfull).
+__global__ void __launch_bounds__(kThreads) k_block_argmin_i32_vec(const int32_t* __restrict__ A,
+                                                                   uint64_t nfull, uint32_t k,
+                                                                   uint64_t* __restrict__ keys) {
+    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (blk >= nfull) return;
+    const unsigned lane = lane_id();
+    const uint32_t base_pos = uint32_t(blk * k);
+    const int4* v4 = reinterpret_cast<const int4*>(A + uint64_t(base_pos));
+    const uint32_t nvec = k >> 2;  // multiple of 32
+    int32_t bv = 0x7FFFFFFF;
+    uint32_t bp = 0xFFFFFFFFu;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+        int4 x[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (v0 + 32 * u < nvec) x[u] = ld_stream_v4(v4 + v0 + 32 * u + lane);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            const uint32_t p = base_pos + 4 * (v0 + 32 * u + lane);
+            // ascending positions + strict '<' => lane-local leftmost minimum;
+            // the (bp == ~0) test seeds the first element even if it is INT32_MAX.
+            if (x[u].x < bv || bp == 0xFFFFFFFFu) { bv = x[u].x; bp = p; }
+            if (x[u].y < bv) { bv = x[u].y; bp = p + 1; }
+            if (x[u].z < bv) { bv = x[u].z; bp = p + 2; }
+            if (x[u].w < bv) { bv = x[u].w; bp = p + 3; }
+        }
+    }
+    const uint64_t key = warp_min_key(pack_key(bv, bp));
+    if (lane == 0) keys[blk] = key;
+}
+
+// Any k / alignment: warp per block, lane-strided coalesced scalar loads.
+__global__ void __launch_bounds__(kThreads) k_block_argmin_i32_gen(const int32_t* __restrict__ A,
+                                                                   uint64_t n, uint32_t k,
+                                                                   uint64_t first, uint64_t nblk,
+                                                                   uint64_t* __restrict__ keys) {
+    const uint64_t blk = first + ((uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5);
+    if (blk >= nblk) return;
+    const unsigned lane = lane_id();
+    const uint64_t lo = blk * k;
+    const uint64_t hi = lo + k < n ? lo + k : n;
+    uint64_t best = kNoKey;
+    for (uint64_t i = lo + lane; i < hi; i += 32) best = kmin(best, pack_key(__ldg(A + i), uint32_t(i)));
+    best = warp_min_key(best);
+    if (lane == 0) keys[blk] = best;
+}
+
+// Packed-key input (A_Q).  Device-side length: blocks past ceil(len/k) exit.
+__global__ void __launch_bounds__(kThreads) k_block_argmin_keys(const uint64_t* __restrict__ K,
+                                                                uint64_t len_max,
+                                                                const uint64_t* __restrict__ len_dev,
+                                                                uint32_t k,
+                                                                uint64_t* __restrict__ keys,
+                                                                uint64_t* __restrict__ b_dev) {
+    const uint64_t len = len_dev ? *len_dev : len_max;
+    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
+    const uint64_t lo = blk * k;
+    if (lo >= len) return;
+    const unsigned lane = lane_id();
+    const uint64_t hi = lo + k < len ? lo + k : len;
+    uint64_t best = kNoKey;
+    if ((k & 63u) == 0 && hi - lo == k && (reinterpret_cast<uintptr_t>(K) & 15u) == 0) {
+        const uint4* v4 = reinterpret_cast<const uint4*>(K + lo);
+        const uint32_t nvec = k >> 1;  // multiple of 32
+        for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+            uint4 x[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                if (v0 + 32 * u < nvec) x[u] = ld_stream_u4(v4 + v0 + 32 * u + lane);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                if (v0 + 32 * u >= nvec) break;
+                best = kmin(best, (uint64_t(x[u].y) << 32) | x[u].x);
+                best = kmin(best, (uint64_t(x[u].w) << 32) | x[u].z);
+            }
+        }
+    } else {
+        for (uint64_t i = lo + lane; i < hi; i += 32) best = kmin(best, __ldg(K + i));
+    }
+    best = warp_min_key(best);
+    if (lane == 0) keys[blk] = best;
+}
+
+inline unsigned grid_for_warps(uint64_t warps) {
+    return unsigned((warps + kWarps - 1) / kWarps);
+}
+
+}  // namespace
+
+int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
+                            cudaStream_t stream) {
+    const uint64_t nblk = (n + k - 1) / k;
+    if (nblk == 0) return 0;
+    int launches = 0;
+    uint64_t done = 0;
+    if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
+        const uint64_t nfull = n / k;
+        if (nfull) {
+            k_block_argmin_i32_vec<<<grid_for_warps(nfull), kThreads, 0, stream>>>(A, nfull, k, keys);
+            ++launches;
+        }
+        done = nfull;
+    }
+    if (done < nblk) {
+        k_block_argmin_i32_gen<<<grid_for_warps(nblk - done), kThreads, 0, stream>>>(A, n, k, done,
+                                                                                     nblk, keys);
+        ++launches;
+    }
+    return launches;
+}
+
+int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
+                             uint32_t k, uint64_t* keys, uint64_t* b_dev, cudaStream_t stream) {
+    uint64_t nblk = (len_max + k - 1) / k;
+    if (nblk == 0) nblk = 1;  // still publish *b_dev
+    k_block_argmin_keys<<<grid_for_warps(nblk), kThreads, 0, stream>>>(K, len_max, len_dev, k, keys,
+                                                                       b_dev);
+    return 1;
+}
+
+}  // namespace brmq

@@ -1,0 +1,472 @@
+// contract.cu -- BbST_CON stages 1-2 on the device: endpoints, dedup/rank,
+// and the segmented argmin that contracts A into A_Q.
+//
+// Reference stages replaced:
+//   collect_endpoints          contraction.cpp:13-23
+//   dedup -> boundary          contraction.cpp:118-127
+//   scan_areas / build_contracted   contraction.cpp:81-151 (inclusive areas)
+//   remap_queries_from_sorted  contraction.cpp:174-199
+//
+// B200 design.  The boundary set is handed to the contraction kernel as a
+// bitmap over A (bit p set <=> p is a query endpoint), so a tile of A finds
+// its area boundaries with one coalesced 512-byte read instead of a search
+// in the sorted boundary list.  The contraction kernel is ONE streaming pass
+// over A[b_0 .. b_last]: each CTA owns a 4096-element tile (16 elements per
+// thread), computes per thread (boundary count, open-segment min), runs a
+// block-wide segmented-min + sum scan, publishes the tile aggregate and
+// resolves the segment that enters the tile from the left with a decoupled
+// look-back over epoch-tagged tile descriptors.  A second walk over the
+// registers then writes each finished area as a packed key (value, leftmost
+// A position), i.e. aq_values and aq_origin in one 8-byte word.  Area t is
+// closed with the boundary element A[b_{t+1}] that opens area t+1, which
+// restores the reference's inclusive-both-ends areas (contraction.hpp:25-27)
+// with every element read once.  The kernel clears the bitmap words it
+// consumed, so the bitmap never needs a memset.
+//
+// Two ways to produce the bitmap + query ranks (BRMQ_SORT_* in brmq.h):
+//   radix  : k_collect -> device radix sort (radix_sort.cu) -> k_unique
+//            (dedup, ranks = cleft / cright, marks the bitmap)
+//   bitmap : k_collect marks the bitmap directly (a counting sort by
+//            position with one presence bit per key); ranks come afterwards
+//            from per-word prefix counts the contraction kernel emits.
+#include "common.cuh"
+#include "kernels.h"
+#include "scan.cuh"
+
+namespace brmq {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;  // 4096
+
+// ------------------------------------------------------------------ collect
+// span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
+__global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restrict__ Q, uint64_t q,
+                                                      uint64_t n, uint32_t* __restrict__ keys,
+                                                      uint32_t* __restrict__ vals,
+                                                      uint32_t* __restrict__ bitmap,
+                                                      uint32_t* __restrict__ span,
+                                                      uint32_t* __restrict__ err) {
+    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    if (i < q) {
+        const ulonglong2 x = __ldg(Q + i);
+        uint64_t l = x.x, r = x.y;
+        if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
+        if (r >= n) {                                        // naive.hpp:14-15 (range)
+            atomicOr(err, 2u);
+            r = n - 1;
+            if (l > r) l = r;
+        }
+        lo = uint32_t(l);
+        hi = uint32_t(r);
+        if (keys) {
+            reinterpret_cast<uint2*>(keys)[i] = make_uint2(lo, hi);
+            reinterpret_cast<uint2*>(vals)[i] =
+                make_uint2(uint32_t(i << 1), uint32_t((i << 1) | 1u));  // contraction.hpp:16-18
+        }
+        if (bitmap) {
+            atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
+            atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
+        }
+    }
+    if (span) {
+        const uint32_t wlo = __reduce_min_sync(kFull, lo);
+        const uint32_t whi = __reduce_max_sync(kFull, hi);
+        if (lane_id() == 0 && wlo != 0xFFFFFFFFu) {
+            atomicMax(span + 0, ~wlo);
+            atomicMax(span + 1, whi);
+        }
+    }
+}
+
+// ------------------------------------------------------------------- unique
+// Sorted endpoints -> ranks.  rank(j) = (#distinct positions among 0..j) - 1.
+__global__ void __launch_bounds__(kThreads) k_unique(
+    const uint32_t* __restrict__ pos, const uint32_t* __restrict__ org, uint64_t m, uint64_t n,
+    uint32_t* __restrict__ boundary, uint32_t* __restrict__ cleft, uint32_t* __restrict__ cright_raw,
+    uint32_t* __restrict__ bitmap, uint32_t* __restrict__ span, uint64_t* __restrict__ nb_out,
+    uint32_t* __restrict__ err, uint64_t* __restrict__ status, uint32_t* __restrict__ ticket,
+    uint32_t epoch) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_scan[kThreads / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * kTile + uint64_t(threadIdx.x) * kItems;
+
+    uint32_t p[kItems];
+    if (base + kItems <= m) {
+        const uint4* v = reinterpret_cast<const uint4*>(pos + base);
+#pragma unroll
+        for (int j = 0; j < kItems / 4; ++j) {
+            const uint4 x = __ldg(v + j);
+            p[4 * j] = x.x; p[4 * j + 1] = x.y; p[4 * j + 2] = x.z; p[4 * j + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) p[j] = base + j < m ? __ldg(pos + base + j) : 0u;
+    }
+    uint32_t prev = base > 0 && base - 1 < m ? __ldg(pos + base - 1) : 0u;
+    uint32_t heads = 0, cnt = 0;
+    bool unsorted = false;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const uint64_t idx = base + j;
+        if (idx < m) {
+            const bool h = idx == 0 || p[j] != prev;
+            unsorted |= idx > 0 && p[j] < prev;            // contraction.cpp:123
+            heads |= uint32_t(h) << j;
+            cnt += h;
+            prev = p[j];
+        }
+    }
+    if (unsorted) atomicOr(err, 4u);
+    uint32_t total;
+    const uint32_t excl = block_excl_sum<kThreads>(cnt, s_scan, total);
+    if (threadIdx.x == 0) {
+        if (tile == 0) {
+            st_relaxed_u64(status, status_pack(epoch, kStInclusive, false, total));
+            s_excl = 0;
+        } else {
+            st_relaxed_u64(status + tile, status_pack(epoch, kStAggregate, false, total));
+            const uint64_t e = lookback_sum(status, tile, epoch);
+            st_relaxed_u64(status + tile, status_pack(epoch, kStInclusive, false, e + total));
+            s_excl = e;
+        }
+    }
+    __syncthreads();
+    uint64_t r = s_excl + excl;  // rank of the next head; item rank = r - 1 after its head
+    uint4 o4[kItems / 4];
+    if (base + kItems <= m && cleft) {
+        const uint4* v = reinterpret_cast<const uint4*>(org + base);
+#pragma unroll
+        for (int j = 0; j < kItems / 4; ++j) o4[j] = __ldg(v + j);
+    }
+    const uint32_t* o = reinterpret_cast<const uint32_t*>(o4);
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const uint64_t idx = base + j;
+        if (idx >= m) break;
+        if ((heads >> j) & 1u) {
+            ++r;
+            if (p[j] >= n) atomicOr(err, 2u);  // position past the array: range error
+            else if (bitmap) atomicOr(bitmap + (p[j] >> 5), 1u << (p[j] & 31));
+            if (boundary) boundary[r - 1] = p[j];
+        }
+        if (cleft) {
+            const uint32_t og = base + kItems <= m ? o[j] : __ldg(org + idx);
+            const uint32_t qi = og >> 1;
+            ((og & 1u) ? cright_raw : cleft)[qi] = uint32_t(r - 1);
+        }
+        if (idx == 0 && span) span[0] = ~p[j];
+        if (idx == m - 1) {
+            *nb_out = r;
+            if (span) span[1] = p[j];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- contract
+__device__ __forceinline__ uint64_t wait_acquire(const uint64_t* status, uint64_t t, uint32_t epoch) {
+    uint64_t s;
+    while (true) {
+        s = ld_acquire_u64(status + t);
+        if (status_state(s, epoch) != kStInvalid) break;
+        __nanosleep(32);
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) k_contract(
+    const int32_t* __restrict__ A, uint64_t n, uint32_t* __restrict__ bitmap,
+    const uint32_t* __restrict__ span, uint64_t* __restrict__ status, uint64_t* __restrict__ key_agg,
+    uint64_t* __restrict__ key_inc, uint32_t* __restrict__ ticket, uint32_t epoch,
+    uint64_t* __restrict__ aq, uint64_t* __restrict__ aq_len, uint64_t* __restrict__ nb_out,
+    uint2* __restrict__ word_info) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t shk[kThreads / 32 + 1];
+    __shared__ uint32_t shf[kThreads / 32 + 1], shc[kThreads / 32 + 1];
+    __shared__ unsigned long long s_excl;
+    __shared__ uint64_t s_carry;
+
+    const uint32_t b0 = ~span[0], blast = span[1];
+    if (b0 > blast) return;  // no endpoints
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint64_t tfirst = b0 / kTile, tlast = blast / kTile;
+    const uint64_t t = tfirst + s_tile;
+    if (t > tlast) return;
+    const uint64_t p0 = t * kTile + uint64_t(threadIdx.x) * kItems;
+
+    // boundary flags for this thread's 16 positions (two threads share a word)
+    uint32_t word = 0;
+    if (p0 < n) word = bitmap[p0 >> 5];
+    const uint32_t fl = (word >> (p0 & 31)) & 0xFFFFu;
+
+    // the thread's 16 elements; positions outside [b0, blast] are not in any area
+    const bool any = p0 <= blast && p0 + kItems - 1 >= b0;
+    int32_t v[kItems];
+    if (any) {
+        if (p0 + kItems <= n && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
+            const int4* a4 = reinterpret_cast<const int4*>(A + p0);
+#pragma unroll
+            for (int j = 0; j < kItems / 4; ++j) {
+                const int4 x = __ldg(a4 + j);
+                v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kItems; ++j) v[j] = p0 + j < n ? __ldg(A + p0 + j) : 0;
+        }
+    }
+    // pass 1: count and the min of the segment open at the thread's right end
+    uint64_t run = kNoKey;
+    if (any) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const uint64_t p = p0 + j;
+            if (p < b0 || p > blast) continue;
+            const uint64_t key = pack_key(v[j], uint32_t(p));
+            run = ((fl >> j) & 1u) ? key : kmin(run, key);
+        }
+    }
+    const uint32_t cnt = __popc(fl);
+    SegMin xe, xt;
+    uint32_t ce, ct;
+    block_excl_segmin_sum<kThreads>(SegMin{run, cnt != 0}, cnt, xe, ce, xt, ct, shk, shf, shc);
+
+    // tile descriptor + decoupled look-back (thread 0)
+    if (threadIdx.x == 0) {
+        if (t == tfirst) {  // first tile starts with b0: nothing enters from the left
+            key_inc[t] = xt.k;
+            st_release_u64(status + t, status_pack(epoch, kStInclusive, xt.f, ct));
+            s_excl = 0;
+            s_carry = kNoKey;
+        } else {
+            key_agg[t] = xt.k;
+            st_release_u64(status + t, status_pack(epoch, kStAggregate, xt.f, ct));
+            uint64_t excl = 0, carry = kNoKey;
+            bool key_done = false;
+            uint64_t p = t;
+            while (p > tfirst) {
+                --p;
+                const uint64_t s = wait_acquire(status, p, epoch);
+                excl += status_value(s);
+                if (status_state(s, epoch) == kStInclusive) {
+                    if (!key_done) carry = kmin(carry, ld_relaxed_u64(key_inc + p));
+                    break;
+                }
+                if (!key_done) {
+                    carry = kmin(carry, ld_relaxed_u64(key_agg + p));
+                    key_done = status_flag(s);
+                }
+            }
+            key_inc[t] = xt.f ? xt.k : kmin(carry, xt.k);
+            st_release_u64(status + t, status_pack(epoch, kStInclusive, false, excl + ct));
+            s_excl = excl;
+            s_carry = carry;
+        }
+    }
+    __syncthreads();
+
+    // pass 2: write the areas closed inside this thread
+    uint64_t cur = xe.f ? xe.k : kmin(s_carry, xe.k);
+    uint64_t rank = s_excl + ce;  // boundaries strictly before p0
+    if (any) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const uint64_t p = p0 + j;
+            if (p < b0 || p > blast) continue;
+            const uint64_t key = pack_key(v[j], uint32_t(p));
+            if ((fl >> j) & 1u) {
+                if (rank > 0) aq[rank - 1] = kmin(cur, key);  // close area rank-1 with A[b]
+                ++rank;
+                cur = key;                                     // b opens the next area
+            } else {
+                cur = kmin(cur, key);
+            }
+        }
+    }
+    // consumed bitmap words: hand out (prefix, bits) for the remap, then clear
+    if ((p0 & 31) == 0 && word != 0) {
+        if (word_info) word_info[p0 >> 5] = make_uint2(uint32_t(s_excl + ce), word);
+        bitmap[p0 >> 5] = 0;
+    }
+    if (t == tlast && threadIdx.x == 0) {
+        const uint64_t nb = s_excl + ct;
+        *nb_out = nb;
+        *aq_len = nb - 1;
+    }
+}
+
+// ------------------------------------------------------------ bitmap remap
+__global__ void __launch_bounds__(kThreads) k_remap_bitmap(const ulonglong2* __restrict__ Q,
+                                                           uint64_t q, uint64_t n,
+                                                           const uint2* __restrict__ word_info,
+                                                           uint32_t* __restrict__ cleft,
+                                                           uint32_t* __restrict__ cright_raw) {
+    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(Q + i);
+    uint64_t l = x.x, r = x.y;
+    if (l > r) { const uint64_t t = l; l = r; r = t; }
+    if (r >= n) { r = n - 1; if (l > r) l = r; }
+    const uint2 wl = __ldg(word_info + (l >> 5)), wr = __ldg(word_info + (r >> 5));
+    cleft[i] = wl.x + __popc(wl.y & ((1u << (l & 31)) - 1u));
+    cright_raw[i] = wr.x + __popc(wr.y & ((1u << (r & 31)) - 1u));
+}
+
+// --------------------------------------------------- stage-API helper kernels
+__global__ void k_split_eps(const uint2* __restrict__ eps, uint64_t m, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) {
+        const uint2 e = eps[i];
+        keys[i] = e.x;
+        vals[i] = e.y;
+    }
+}
+__global__ void k_join_eps(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                           uint64_t m, uint2* __restrict__ eps) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) eps[i] = make_uint2(keys[i], vals[i]);
+}
+__global__ void k_split_aq(const uint64_t* __restrict__ aq, const uint64_t* __restrict__ len,
+                           uint64_t len_max, int32_t* __restrict__ values,
+                           uint64_t* __restrict__ origin) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < len_max && i < *len) {
+        values[i] = key_value(aq[i]);
+        origin[i] = key_pos(aq[i]);
+    }
+}
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, const uint64_t* __restrict__ len,
+                             uint64_t len_max, uint64_t* __restrict__ out) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < len_max && i < *len) out[i] = a[i];
+}
+// remap_queries_from_sorted semantics by binary search in the boundary list
+// (contraction.cpp:153-199): missing endpoint -> err |= 8 (logic_error).
+__global__ void k_remap_search(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ org,
+                               uint64_t m, const uint64_t* __restrict__ boundary, uint64_t nb,
+                               uint64_t q, uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
+                               uint32_t* __restrict__ err) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t p = pos[i];
+    uint64_t lo = 0, hi = nb;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (boundary[mid] < p) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t og = org[i];
+    if (lo >= nb || boundary[lo] != p || (og >> 1) >= q) {
+        atomicOr(err, 8u);
+        return;
+    }
+    ((og & 1u) ? cr : cl)[og >> 1] = uint32_t(lo);
+}
+__global__ void k_remap_finish(uint64_t q, const uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
+                               uint8_t* __restrict__ dg) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    if (cr[i] == cl[i]) dg[i] = 1;  // contraction.cpp:191-197
+    else { dg[i] = 0; cr[i] -= 1; }
+}
+__global__ void k_keys_to_pos(uint64_t* __restrict__ t, uint64_t count) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < count) t[i] = t[i] == kNoKey ? ~0ull : uint64_t(key_pos(t[i]));
+}
+
+inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
+                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s) {
+    if (q == 0) return 0;
+    k_collect<<<g256(q), kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
+                                           bitmap, span, err);
+    return 1;
+}
+
+size_t unique_status_words(uint64_t m) { return (m + kTile - 1) / kTile; }
+
+int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n, uint32_t* boundary,
+                  uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* span,
+                  uint64_t* nb_out, uint32_t* err, uint64_t* status, uint32_t* ticket,
+                  uint32_t epoch, cudaStream_t s) {
+    if (m == 0) return 0;
+    k_unique<<<unsigned((m + kTile - 1) / kTile), kThreads, 0, s>>>(
+        pos, org, m, n, boundary, cleft, cright_raw, bitmap, span, nb_out, err, status, ticket, epoch);
+    return 1;
+}
+
+size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
+
+int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
+                    uint64_t* status, uint64_t* key_agg, uint64_t* key_inc, uint32_t* ticket,
+                    uint32_t epoch, uint64_t* aq, uint64_t* aq_len, uint64_t* nb_out,
+                    uint2* word_info, cudaStream_t s) {
+    if (n == 0) return 0;
+    k_contract<<<unsigned(contract_tiles(n)), kThreads, 0, s>>>(
+        A, n, bitmap, span, status, key_agg, key_inc, ticket, epoch, aq, aq_len, nb_out, word_info);
+    return 1;
+}
+
+int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
+                        uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s) {
+    if (q == 0) return 0;
+    k_remap_bitmap<<<g256(q), kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n,
+                                                word_info, cleft, cright_raw);
+    return 1;
+}
+
+int launch_split_eps(const void* eps, uint64_t m, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (!m) return 0;
+    k_split_eps<<<g256(m), 256, 0, s>>>(static_cast<const uint2*>(eps), m, keys, vals);
+    return 1;
+}
+int launch_join_eps(const uint32_t* keys, const uint32_t* vals, uint64_t m, void* eps,
+                    cudaStream_t s) {
+    if (!m) return 0;
+    k_join_eps<<<g256(m), 256, 0, s>>>(keys, vals, m, static_cast<uint2*>(eps));
+    return 1;
+}
+int launch_split_aq(const uint64_t* aq, const uint64_t* len, uint64_t len_max, int32_t* values,
+                    uint64_t* origin, cudaStream_t s) {
+    if (!len_max) return 0;
+    k_split_aq<<<g256(len_max), 256, 0, s>>>(aq, len, len_max, values, origin);
+    return 1;
+}
+int launch_u32_to_u64(const uint32_t* a, const uint64_t* len, uint64_t len_max, uint64_t* out,
+                      cudaStream_t s) {
+    if (!len_max) return 0;
+    k_u32_to_u64<<<g256(len_max), 256, 0, s>>>(a, len, len_max, out);
+    return 1;
+}
+int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
+                        const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cl,
+                        uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s) {
+    int l = 0;
+    if (m) {
+        k_remap_search<<<g256(m), 256, 0, s>>>(pos, org, m, boundary, nb, q, cl, cr, err);
+        ++l;
+    }
+    if (q) {
+        k_remap_finish<<<g256(q), 256, 0, s>>>(q, cl, cr, dg);
+        ++l;
+    }
+    return l;
+}
+int launch_keys_to_pos(uint64_t* t, uint64_t count, cudaStream_t s) {
+    if (!count) return 0;
+    k_keys_to_pos<<<g256(count), 256, 0, s>>>(t, count);
+    return 1;
+}
+
+}  // namespace brmq

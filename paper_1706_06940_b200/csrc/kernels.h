@@ -1,0 +1,75 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (one .cu per stage).
+// All launchers are asynchronous on the given stream and return the number of
+// kernel launches they issued (for the bench's gpu_launches count).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace brmq {
+
+// ---------------------------------------------------------------- block_argmin.cu
+// Level 0 of the block Sparse Table: keys[j] = packed leftmost-min key of block j
+// (SPEC.md:199-203).
+int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
+                            cudaStream_t stream);
+// Same over packed keys (A_Q) whose true length *len_dev <= len_max lives on the
+// device; also stores *b_dev = ceil(len / k) for the later stages.
+int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
+                             uint32_t k, uint64_t* keys, uint64_t* b_dev, cudaStream_t stream);
+
+// ---------------------------------------------------------------- sparse_table.cu
+// Levels 1..L-1 of the block Sparse Table, row e at ST + e*b (row 0 = level 0).
+// b_dev (nullable) holds the true block count <= b (rows stay strided by b).
+int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStream_t stream);
+
+// ---------------------------------------------------------------- query.cu
+int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST,
+                        uint64_t b, const uint64_t* Q, uint64_t q, uint64_t* answers,
+                        uint32_t* err, cudaStream_t stream);
+int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint32_t k,
+                            const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
+                            const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,
+                            uint64_t* answers, cudaStream_t stream);
+
+// ---------------------------------------------------------------- radix_sort.cu
+size_t radix_sort_temp_bytes(uint64_t m, int bits);
+int radix_sort_passes(int bits);
+// Stable LSD sort of (key, value) u32 pairs by the low `bits` key bits; uses
+// epochs epoch_base .. epoch_base + passes - 1.  *result_in_alt tells whether
+// the sorted data ended in alt_keys / alt_vals.
+int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
+                      uint64_t m, int bits, void* tmp, cudaStream_t stream, bool* result_in_alt,
+                      uint32_t epoch_base);
+
+// ---------------------------------------------------------------- contract.cu
+int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
+                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s);
+size_t unique_status_words(uint64_t m);
+int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
+                  uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
+                  uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
+                  uint32_t* ticket, uint32_t epoch, cudaStream_t s);
+size_t contract_tiles(uint64_t n);
+int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
+                    uint64_t* status, uint64_t* key_agg, uint64_t* key_inc, uint32_t* ticket,
+                    uint32_t epoch, uint64_t* aq, uint64_t* aq_len, uint64_t* nb_out,
+                    uint2* word_info, cudaStream_t s);
+int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
+                        uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
+// stage-API helpers (not on the solve path)
+int launch_split_eps(const void* eps, uint64_t m, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+int launch_join_eps(const uint32_t* keys, const uint32_t* vals, uint64_t m, void* eps,
+                    cudaStream_t s);
+int launch_split_aq(const uint64_t* aq, const uint64_t* len, uint64_t len_max, int32_t* values,
+                    uint64_t* origin, cudaStream_t s);
+int launch_u32_to_u64(const uint32_t* a, const uint64_t* len, uint64_t len_max, uint64_t* out,
+                      cudaStream_t s);
+int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
+                        const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cl,
+                        uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s);
+int launch_keys_to_pos(uint64_t* t, uint64_t count, cudaStream_t s);
+
+}  // namespace brmq

@@ -1,0 +1,285 @@
+// query.cu -- speculative query answering over the block Sparse Table (K3).
+//
+// SPEC.md:219-236 (inner_span_min + answer_one), PAPER.md:242-255 (BbST_CON
+// stage 4) and PAPER.md:301-327 (BbST), with the leftmost-exact speculation
+// rule of SURVEY 0.5/7 (SPEC's literal "scan only if stored min < best" is
+// value-exact but not position-exact under ties):
+//   inner span  : blocks bl+1..br-1 via two ST probes at e = floor_log2(br-bl-1)
+//   right block : scan iff (no best || v(R) <  v(best)) and the stored min R lies right of r
+//   left block  : scan iff (no best || v(L) <= v(best)) and the stored min L lies left of l
+//   single block: stored min if it lies in [l, r], else scan [l, r]
+// All candidates are packed keys, so combining them is an unsigned min.
+//
+// B200 design: one lane per query does the O(1) part (4 random 8-byte ST reads,
+// L2-resident for n = 1e8).  Lanes that need a partial-block scan publish it
+// with __ballot_sync and the whole warp scans TPR pending ranges per round:
+// each lane issues VPL predicated 128-bit loads per range (TPR*VPL = 16
+// vectors in flight per lane), only for vectors that overlap the range, and a
+// redux.sync pair reduces each range to its leftmost-min key, which goes back
+// to the owning lane.  No lane idles on the ~70% of queries that need no
+// scan, and partial ranges cost one coalesced round trip per 4 ranges.
+//
+// Two element policies share the kernel: int32 A (key = pack(A[i], i)) for
+// BbST, and packed keys A_Q (key carries the original position, "aq_origin")
+// for BbST_CON.  For A_Q, "stored min lies inside the range" is decided on
+// original positions: aq_origin is non-decreasing, so a block-min
+// key whose origin is >= l (resp. <= r) is present in the partial range.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace brmq {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct ElemI32 {
+    using vec_t = int4;
+    static constexpr int EPV = 4;
+    const int32_t* data;
+    uint64_t len;
+    __device__ __forceinline__ uint64_t key_at(uint64_t i) const {
+        return pack_key(__ldg(data + i), uint32_t(i));
+    }
+    // 128-bit load when the vector lies inside the array, scalar tail otherwise
+    // (never touches memory past `len`; out-of-range lanes are masked later).
+    __device__ __forceinline__ vec_t load_vec(uint64_t v) const {
+        if (v * 4 + 3 < len) return ld_stream_v4(reinterpret_cast<const int4*>(data) + v);
+        int4 x = make_int4(0, 0, 0, 0);
+        if (v * 4 + 0 < len) x.x = __ldg(data + v * 4 + 0);
+        if (v * 4 + 1 < len) x.y = __ldg(data + v * 4 + 1);
+        if (v * 4 + 2 < len) x.z = __ldg(data + v * 4 + 2);
+        return x;
+    }
+    // min key over the elements of vector v that lie in [lo, hi]
+    __device__ __forceinline__ uint64_t vec_min(const vec_t& x, uint64_t v, uint64_t lo,
+                                                uint64_t hi) const {
+        const uint64_t p = v * 4;
+        uint64_t b = kNoKey;
+        if (p + 0 >= lo && p + 0 <= hi) b = kmin(b, pack_key(x.x, uint32_t(p + 0)));
+        if (p + 1 >= lo && p + 1 <= hi) b = kmin(b, pack_key(x.y, uint32_t(p + 1)));
+        if (p + 2 >= lo && p + 2 <= hi) b = kmin(b, pack_key(x.z, uint32_t(p + 2)));
+        if (p + 3 >= lo && p + 3 <= hi) b = kmin(b, pack_key(x.w, uint32_t(p + 3)));
+        return b;
+    }
+};
+
+struct ElemKey {
+    using vec_t = uint4;
+    static constexpr int EPV = 2;
+    const uint64_t* data;  // allocation padded to a multiple of 2 keys by the caller
+    __device__ __forceinline__ uint64_t key_at(uint64_t i) const { return __ldg(data + i); }
+    __device__ __forceinline__ vec_t load_vec(uint64_t v) const {
+        return ld_stream_u4(reinterpret_cast<const uint4*>(data) + v);
+    }
+    __device__ __forceinline__ uint64_t vec_min(const vec_t& x, uint64_t v, uint64_t lo,
+                                                uint64_t hi) const {
+        const uint64_t p = v * 2;
+        uint64_t b = kNoKey;
+        if (p + 0 >= lo && p + 0 <= hi) b = kmin(b, (uint64_t(x.y) << 32) | x.x);
+        if (p + 1 >= lo && p + 1 <= hi) b = kmin(b, (uint64_t(x.w) << 32) | x.z);
+        return b;
+    }
+};
+
+// A query resolved to index coordinates [il, ir] of the scanned array and
+// original-position coordinates [pl, pr] of A (equal for BbST).
+struct Resolved {
+    uint64_t il, ir, pl, pr;
+    uint64_t direct;  // final answer when `done` (degenerate query / range error)
+    bool done;
+};
+
+struct QueryDirect {
+    const uint64_t* Q;
+    uint64_t n;
+    uint32_t* err;
+    __device__ __forceinline__ Resolved resolve(uint64_t i) const {
+        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        uint64_t l = x.x, r = x.y;
+        if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
+        Resolved o{l, r, l, r, 0, false};
+        if (r >= n) {                                        // naive.hpp:14-15
+            atomicOr(err, 1u);
+            o.direct = ~0ull;
+            o.done = true;
+        } else if (l == r) {
+            o.direct = l;
+            o.done = true;
+        }
+        return o;
+    }
+};
+
+struct QueryContracted {
+    const uint64_t* Q;
+    const uint32_t* cleft;
+    const uint32_t* cright_raw;
+    __device__ __forceinline__ Resolved resolve(uint64_t i) const {
+        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        uint64_t l = x.x, r = x.y;
+        if (l > r) { const uint64_t t = l; l = r; r = t; }
+        const uint32_t cl = __ldg(cleft + i), cr = __ldg(cright_raw + i);
+        Resolved o{cl, uint64_t(cr) - 1, l, r, l, cl == cr};  // degenerate: answer = left
+                                                               // (contraction.cpp:192-193)
+        return o;
+    }
+};
+
+template <class E>
+__device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64_t hi) {
+    uint64_t b = kNoKey;
+    for (uint64_t i = lo + lane_id(); i <= hi; i += 32) b = kmin(b, e.key_at(i));
+    return warp_min_key(b);
+}
+
+// VPL vectors per lane cover one block (k = 32 * EPV * VPL); TPR ranges per round.
+template <class E, class QP, int VPL, int TPR>
+__global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
+                                                    const uint64_t* __restrict__ ST,
+                                                    uint64_t stride, uint64_t q,
+                                                    uint64_t* __restrict__ answers) {
+    const unsigned lane = lane_id();
+    const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x);
+    const bool active = i < q;
+
+    uint64_t best = kNoKey, direct = 0;
+    bool done = false, t0 = false, t1 = false;
+    uint64_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+    if (active) {
+        const Resolved rq = qp.resolve(i);
+        direct = rq.direct;
+        done = rq.done;
+        if (!done) {
+            const uint64_t bl = rq.il / k, br = rq.ir / k;
+            const uint64_t L = __ldg(ST + bl);
+            if (bl == br) {
+                if (key_pos(L) >= rq.pl && key_pos(L) <= rq.pr) best = L;
+                else { t0 = true; lo0 = rq.il; hi0 = rq.ir; }
+            } else {
+                if (br - bl >= 2) {  // inner_span_min
+                    const uint32_t e = floor_log2_u64(br - bl - 1);
+                    const uint64_t* row = ST + uint64_t(e) * stride;
+                    best = kmin(__ldg(row + bl + 1), __ldg(row + br - (1ull << e)));
+                }
+                const uint64_t R = __ldg(ST + br);
+                if (best == kNoKey || key_hi(R) < key_hi(best)) {
+                    if (key_pos(R) <= rq.pr) best = kmin(best, R);
+                    else { t1 = true; lo1 = br * k; hi1 = rq.ir; }
+                }
+                if (best == kNoKey || key_hi(L) <= key_hi(best)) {
+                    if (key_pos(L) >= rq.pl) best = kmin(best, L);
+                    else { t0 = true; lo0 = rq.il; hi0 = bl * k + k - 1; }
+                }
+            }
+        }
+    }
+
+    // Warp-cooperative partial-block scans.
+    unsigned m0 = __ballot_sync(kFull, t0), m1 = __ballot_sync(kFull, t1);
+    while (m0 | m1) {
+        uint64_t tlo[TPR > 0 ? TPR : 1], thi[TPR > 0 ? TPR : 1];
+        int src[TPR > 0 ? TPR : 1];
+#pragma unroll
+        for (int u = 0; u < (TPR > 0 ? TPR : 1); ++u) {
+            src[u] = -1;
+            tlo[u] = 0;
+            thi[u] = 0;
+            if (m0) {
+                const int s = __ffs(m0) - 1;
+                m0 &= m0 - 1;
+                src[u] = s;
+                tlo[u] = __shfl_sync(kFull, lo0, s);
+                thi[u] = __shfl_sync(kFull, hi0, s);
+            } else if (m1) {
+                const int s = __ffs(m1) - 1;
+                m1 &= m1 - 1;
+                src[u] = s;
+                tlo[u] = __shfl_sync(kFull, lo1, s);
+                thi[u] = __shfl_sync(kFull, hi1, s);
+            }
+        }
+        if constexpr (VPL == 0) {
+            const uint64_t kk = scan_generic(elem, tlo[0], thi[0]);
+            if (int(lane) == src[0]) best = kmin(best, kk);
+        } else {
+            typename E::vec_t x[TPR][VPL];
+            constexpr int EPV = E::EPV;
+#pragma unroll
+            for (int u = 0; u < TPR; ++u) {
+                const uint64_t vb = (tlo[u] / k) * (k / EPV);  // first vector of the block
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    const uint64_t v = vb + lane + 32 * j;
+                    if (src[u] >= 0 && v * EPV + (EPV - 1) >= tlo[u] && v * EPV <= thi[u])
+                        x[u][j] = elem.load_vec(v);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < TPR; ++u) {
+                if (src[u] < 0) break;  // warp-uniform
+                const uint64_t vb = (tlo[u] / k) * (k / EPV);
+                uint64_t kb = kNoKey;
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    const uint64_t v = vb + lane + 32 * j;
+                    if (v * EPV + (EPV - 1) >= tlo[u] && v * EPV <= thi[u])
+                        kb = kmin(kb, elem.vec_min(x[u][j], v, tlo[u], thi[u]));
+                }
+                kb = warp_min_key(kb);
+                if (int(lane) == src[u]) best = kmin(best, kb);
+            }
+        }
+    }
+    if (active) answers[i] = done ? direct : uint64_t(key_pos(best));
+}
+
+template <class E, class QP, int VPL, int TPR>
+void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
+              uint64_t* ans, cudaStream_t s) {
+    const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
+    k_query<E, QP, VPL, TPR><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans);
+}
+
+template <class QP>
+void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
+                  uint64_t* ans, cudaStream_t s) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0;
+    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 4>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 8>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 2>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 16>(e, qp, k, ST, stride, q, ans, s);
+    return launch_q<ElemI32, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
+}
+
+template <class QP>
+void dispatch_key(ElemKey e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
+                  uint64_t* ans, cudaStream_t s) {
+    if (k == 512) return launch_q<ElemKey, QP, 8, 2>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 256) return launch_q<ElemKey, QP, 4, 4>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 1024) return launch_q<ElemKey, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 128) return launch_q<ElemKey, QP, 2, 8>(e, qp, k, ST, stride, q, ans, s);
+    return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
+}
+
+}  // namespace
+
+int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
+                        const uint64_t* Q, uint64_t q, uint64_t* answers, uint32_t* err,
+                        cudaStream_t stream) {
+    if (q == 0) return 0;
+    dispatch_i32(ElemI32{A, n}, QueryDirect{Q, n, err}, k, ST, b, q, answers, stream);
+    return 1;
+}
+
+int launch_query_contracted(const uint64_t* AQ, const uint64_t* /*aq_len_dev*/, uint32_t k,
+                            const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
+                            const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,
+                            uint64_t* answers, cudaStream_t stream) {
+    if (q == 0) return 0;
+    dispatch_key(ElemKey{AQ}, QueryContracted{Q, cleft, cright_raw}, k, ST, b_max, q, answers,
+                 stream);
+    return 1;
+}
+
+}  // namespace brmq

@@ -1,0 +1,194 @@
+// radix_sort.cu -- on-device LSD radix sort of (pos, origin) endpoint pairs.
+//
+// Replaces radix_sort_by_pos (contraction.cpp:27-63): LSD by 8-bit digits of
+// the 32-bit position, one up-front histogram for every digit (:35-41),
+// stable scatter per pass (:58).  Stability makes the output order identical
+// to the reference's for equal positions (collect order).
+//
+// B200 design (single-pass "onesweep" scheme):
+//   k_rs_hist : one read of the keys builds the histograms of all passes.
+//   k_rs_pass : per pass ONE kernel.  A CTA takes a 4096-key tile (atomic
+//               ticket => tiles start in order), ranks keys stably inside the
+//               warp with __match_any_sync, turns per-warp digit counts into
+//               tile offsets, publishes its 256 digit counts, looks back over
+//               the predecessors' epoch-tagged counts (decoupled look-back,
+//               one thread per digit) and scatters.  No separate scan kernel,
+//               no global barrier, no status clearing between launches.
+// Only ceil(bits/8) passes run, with bits = bit_width(n-1) chosen by the
+// caller (positions < n), e.g. 27 bits -> 4 passes, the last one 3 bits wide.
+#include "common.cuh"
+#include "kernels.h"
+#include "scan.cuh"
+
+namespace brmq {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;  // 4096 keys
+constexpr int kRadix = 256;
+constexpr int kMaxPasses = 4;
+
+__global__ void __launch_bounds__(kThreads) k_rs_hist(const uint32_t* __restrict__ keys, uint64_t m,
+                                                      int passes,
+                                                      unsigned long long* __restrict__ ghist) {
+    __shared__ uint32_t h[kMaxPasses][kRadix];
+    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < m; i += stride) {
+        const uint32_t k = __ldg(keys + i);
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) {
+        const uint32_t c = (&h[0][0])[i];
+        if (c) atomicAdd(ghist + i, (unsigned long long)c);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict__ kin,
+                                                      const uint32_t* __restrict__ vin,
+                                                      uint32_t* __restrict__ kout,
+                                                      uint32_t* __restrict__ vout, uint64_t m,
+                                                      int shift,
+                                                      const unsigned long long* __restrict__ ghist,
+                                                      uint64_t* __restrict__ status,
+                                                      uint32_t* __restrict__ ticket,
+                                                      uint32_t epoch) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t whist[kWarps][kRadix];
+    __shared__ unsigned long long s_base[kRadix];
+    __shared__ uint32_t s_scan[kWarps + 1];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * kTile + uint64_t(warp) * (32 * kItems);
+
+    uint32_t key[kItems], val[kItems], dig[kItems], rank[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const uint64_t idx = base + uint64_t(i) * 32 + lane;
+        const bool ok = idx < m;
+        key[i] = ok ? __ldg(kin + idx) : 0u;
+        val[i] = ok ? __ldg(vin + idx) : 0u;
+        dig[i] = ok ? ((key[i] >> shift) & 0xFFu) : 0x100u;  // 0x100 = no key
+    }
+    // Stable warp-level ranking: item-major, lane-minor == input order.
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const unsigned peers = __match_any_sync(kFull, dig[i]);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t prev = 0;
+        if (dig[i] < 0x100u) prev = whist[warp][dig[i]];
+        __syncwarp();
+        rank[i] = prev + before;
+        if (dig[i] < 0x100u && lane == unsigned(__ffs(peers) - 1))
+            whist[warp][dig[i]] = prev + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Thread d owns digit d: warp offsets, tile count, look-back, global base.
+    const uint32_t d = threadIdx.x;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = whist[w][d];
+        whist[w][d] = sum;
+        sum += c;
+    }
+    uint64_t* st = status + tile * kRadix;
+    if (tile == 0) {
+        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, sum));
+    } else {
+        st_relaxed_u64(st + d, status_pack(epoch, kStAggregate, false, sum));
+    }
+    // Global exclusive digit offsets from the histogram (block scan of 256 counts).
+    const unsigned long long g = ghist[d];
+    // 64-bit exclusive scan via two 32-bit halves is overkill: counts <= 2^32.
+    uint32_t gtot;
+    const uint32_t gex = block_excl_sum<kThreads>(uint32_t(g), s_scan, gtot);
+    uint64_t excl = 0;
+    if (tile > 0) {
+        uint64_t p = tile;
+        while (p > 0) {
+            --p;
+            const uint64_t s = status_wait(status + p * kRadix, d, epoch);
+            excl += status_value(s);
+            if (status_state(s, epoch) == kStInclusive) break;
+        }
+        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, excl + sum));
+    }
+    s_base[d] = (unsigned long long)gex + excl;
+    __syncthreads();
+
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        if (dig[i] < 0x100u) {
+            const uint64_t out = s_base[dig[i]] + whist[warp][dig[i]] + rank[i];
+            kout[out] = key[i];
+            vout[out] = val[i];
+        }
+    }
+}
+
+}  // namespace
+
+size_t radix_sort_temp_bytes(uint64_t m, int bits) {
+    const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
+    const uint64_t tiles = (m + kTile - 1) / kTile;
+    // [ghist: 4*256 u64][tickets: 4 u32 padded to 256 B][status: passes * tiles * 256 u64]
+    return size_t(kMaxPasses * kRadix * 8) + 256 + size_t(passes) * tiles * kRadix * 8;
+}
+
+size_t radix_sort_zero_bytes() { return size_t(kMaxPasses * kRadix * 8) + 256; }
+
+int radix_sort_passes(int bits) { return bits <= 0 ? 0 : (bits + 7) / 8; }
+
+int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
+                      uint64_t m, int bits, void* tmp, cudaStream_t stream, bool* result_in_alt,
+                      uint32_t epoch_base) {
+    *result_in_alt = false;
+    if (m <= 1 || bits <= 0) return 0;
+    const int passes = (bits + 7) / 8;
+    const uint64_t tiles = (m + kTile - 1) / kTile;
+    auto* ghist = static_cast<unsigned long long*>(tmp);
+    auto* tickets = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8);
+    auto* status = reinterpret_cast<uint64_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8 + 256);
+    cudaMemsetAsync(tmp, 0, radix_sort_zero_bytes(), stream);
+    int launches = 0;
+    {
+        uint64_t blocks = (m + kThreads * 8 - 1) / (kThreads * 8);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        k_rs_hist<<<unsigned(blocks), kThreads, 0, stream>>>(keys, m, passes, ghist);
+        ++launches;
+    }
+    const uint32_t* kin = keys;
+    const uint32_t* vin = vals;
+    uint32_t* kout = alt_keys;
+    uint32_t* vout = alt_vals;
+    for (int p = 0; p < passes; ++p) {
+        const uint32_t epoch = epoch_base + uint32_t(p);
+        k_rs_pass<<<unsigned(tiles), kThreads, 0, stream>>>(kin, vin, kout, vout, m, 8 * p,
+                                                            ghist + p * kRadix,
+                                                            status + uint64_t(p) * tiles * kRadix,
+                                                            tickets + p, epoch);
+        ++launches;
+        const uint32_t* tk = kin;
+        const uint32_t* tv = vin;
+        kin = kout;
+        vin = vout;
+        kout = const_cast<uint32_t*>(tk);
+        vout = const_cast<uint32_t*>(tv);
+    }
+    *result_in_alt = (passes & 1) != 0;
+    return launches;
+}
+
+}  // namespace brmq

@@ -1,0 +1,286 @@
+"""Parity of the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: bit-exact leftmost-minimum positions (integer work).  The oracle is the
+reference's own code compiled under oracle/_ref when present (it travels with
+the gpurun snapshot) and the C restatement oracle/liboracle.so otherwise; for
+small cases a pure-numpy argmin is checked too.
+"""
+import numpy as np
+import pytest
+
+from paper_1706_06940_b200 import (ENDPOINT_DTYPE, InvalidArgument, LogicError, OutOfRange,
+                                   SortKind, make_queries)
+
+pytestmark = pytest.mark.gpu
+
+KS = [1, 2, 3, 7, 8, 64, 128, 256, 512, 1024, 2048, 4096]
+VARIANTS = ["bbst", "con_radix", "con_bitmap"]
+
+
+def _values(r, n, kind):
+    if kind == "uniform":
+        return r.integers(0, 2**31, n, dtype=np.int64).astype(np.int32)
+    if kind == "binary":
+        return r.integers(0, 2, n).astype(np.int32)
+    if kind == "ties16":
+        return r.integers(0, 16, n).astype(np.int32)
+    if kind == "signed":
+        v = r.integers(-(2**31), 2**31, n, dtype=np.int64).astype(np.int32)
+        v[r.integers(0, n, max(1, n // 50))] = np.iinfo(np.int32).min
+        v[r.integers(0, n, max(1, n // 50))] = np.iinfo(np.int32).max
+        return v
+    if kind == "const_max":
+        return np.full(n, np.iinfo(np.int32).max, np.int32)
+    if kind == "walk":
+        s = np.cumsum(np.where(r.integers(0, 2, n) == 1, 1, -1)).astype(np.int64)
+        return (s - s.min()).astype(np.int32)
+    raise ValueError(kind)
+
+
+def _queries(r, n, q, kind):
+    if kind == "uniform":
+        a, b = r.integers(0, n, q), r.integers(0, n, q)
+    elif kind == "short":
+        a = r.integers(0, n, q)
+        b = np.minimum(a + r.integers(0, 40, q), n - 1)
+    elif kind == "mixed":
+        a = r.integers(0, n, q)
+        ln = np.where(r.random(q) < 0.5, r.integers(1, 700, q), r.integers(1, n + 1, q))
+        b = np.minimum(a + ln - 1, n - 1)
+    elif kind == "degenerate":
+        a = r.integers(0, n, q)
+        b = a.copy()
+    elif kind == "reversed":
+        a, b = r.integers(0, n, q), r.integers(0, n, q)
+        Q = np.empty((q, 2), np.uint64)
+        Q[:, 0], Q[:, 1] = np.maximum(a, b), np.minimum(a, b)  # left > right: normalised
+        return Q
+    else:
+        raise ValueError(kind)
+    return np.stack([np.minimum(a, b), np.maximum(a, b)], 1).astype(np.uint64)
+
+
+def _solve(engine, variant, A, Q, k):
+    if variant == "bbst":
+        return engine.solve_batch_bbst(A, Q, k)
+    kind = SortKind.Radix if variant == "con_radix" else SortKind.Bitmap
+    return engine.solve_batch_bbst_con(A, Q, k, kind)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("vkind", ["uniform", "binary", "ties16", "signed", "const_max", "walk"])
+def test_random_small_all_k(engine, orc, variant, vkind):
+    r = np.random.default_rng(hash((variant, vkind)) % 2**32)
+    for trial in range(6):
+        n = int(r.integers(1, 6000))
+        q = int(r.integers(1, 1500))
+        A = _values(r, n, vkind)
+        qk = ["uniform", "short", "mixed", "degenerate", "reversed", "uniform"][trial]
+        Q = _queries(r, n, q, qk)
+        want = orc.naive_numpy(A, Q)
+        for k in KS:
+            got = _solve(engine, variant, A, Q, k)
+            bad = np.nonzero(got != want)[0]
+            assert bad.size == 0, (variant, vkind, qk, n, q, k, bad[:5], got[bad[:5]], want[bad[:5]])
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_spec_worked_instance(engine, variant):
+    # A=[5,3,8,2,7,6,9,1], queries (1,4),(3,6) -> [3,3]
+    A = np.array([5, 3, 8, 2, 7, 6, 9, 1], np.int32)
+    Q = make_queries([1, 3], [4, 6])
+    for k in (1, 2, 3, 512):
+        assert list(_solve(engine, variant, A, Q, k)) == [3, 3]
+    # SPEC.md:64-66, 82-84
+    assert list(_solve(engine, variant, np.array([7], np.int32), make_queries([0], [0]), 512)) == [0]
+    assert list(_solve(engine, variant, np.array([2, 2, 2], np.int32), make_queries([0], [2]), 2)) == [0]
+    assert list(_solve(engine, variant, A, make_queries([0, 4], [7, 4]), 2)) == [7, 4]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_edge_cases(engine, orc, variant):
+    A = np.arange(100, 0, -1, dtype=np.int32)
+    # empty batch -> empty answers
+    assert _solve(engine, variant, A, np.zeros((0, 2), np.uint64), 512).shape == (0,)
+    # all queries identical
+    Q = np.tile(np.array([[10, 90]], np.uint64), (777, 1))
+    assert (_solve(engine, variant, A, Q, 8) == 90).all()
+    # full-range and single-element arrays
+    assert list(_solve(engine, variant, np.array([5], np.int32), make_queries([0], [0]), 1)) == [0]
+    # out of range -> std::out_of_range
+    with pytest.raises(OutOfRange):
+        _solve(engine, variant, A, make_queries([0], [100]), 512)
+    # k = 0 -> invalid_argument (BbstConParams invariant k >= 1)
+    with pytest.raises(InvalidArgument):
+        _solve(engine, variant, A, make_queries([0], [5]), 0)
+    # the engine is still healthy after an error
+    assert list(_solve(engine, variant, A, make_queries([3], [9]), 4)) == [9]
+
+
+def test_device_pointers(engine, orc):
+    torch = pytest.importorskip("torch")
+    r = np.random.default_rng(7)
+    A = _values(r, 200_000, "ties16")
+    Q = _queries(r, 200_000, 50_000, "mixed")
+    want = orc.solve_oracle(A, Q)
+    dA = torch.from_numpy(A).cuda()
+    dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+    for variant in VARIANTS:
+        if variant == "bbst":
+            out = engine.solve_batch_bbst(dA, dQ, 512)
+        else:
+            out = engine.solve_batch_bbst_con(dA, dQ, 512,
+                                              SortKind.Radix if variant == "con_radix" else SortKind.Bitmap)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), variant
+
+
+# ------------------------------------------------------------------ stage parity
+def test_stage_collect_sort(engine, orc):
+    import ctypes as C
+    r = np.random.default_rng(11)
+    for q in (0, 1, 5, 31, 32, 33, 1000, 100_000):
+        n = 1_000_003
+        Q = _queries(r, n, q, "uniform")
+        eps = engine.collect_endpoints(Q)
+        want = np.empty(2 * q, ENDPOINT_DTYPE)
+        orc.port().orc_collect_endpoints(orc._p(Q), q, orc._p(want))
+        assert np.array_equal(eps, want)
+        # device radix sort is stable: identical to the reference Radix order
+        got = engine.sort_endpoints(eps.copy())
+        ref = want.copy()
+        if orc.ref_available():
+            orc.ref().ref_sort_endpoints(orc._p(ref), 2 * q, 0)
+        else:
+            orc.port().orc_sort_endpoints(orc._p(ref), 2 * q, 0)
+        if 2 * q >= 64:
+            assert np.array_equal(got, ref), q
+        else:  # reference uses std::sort below 64 endpoints: order of equal pos unspecified
+            assert np.array_equal(got["pos"], ref["pos"])
+            assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(ref.view(np.uint64)))
+    # full 32-bit keys
+    e = np.empty(50_000, ENDPOINT_DTYPE)
+    e["pos"] = r.integers(0, 2**32, e.shape[0], dtype=np.uint64).astype(np.uint32)
+    e["origin"] = np.arange(e.shape[0], dtype=np.uint32)
+    got = engine.sort_endpoints(e.copy())
+    order = np.argsort(e["pos"], kind="stable")
+    assert np.array_equal(got, e[order])
+
+
+def test_stage_contract_remap(engine, orc):
+    r = np.random.default_rng(12)
+    for n, q, vk in [(1, 1, "uniform"), (50, 3, "binary"), (10_000, 100, "ties16"),
+                     (300_000, 20_000, "uniform"), (100_000, 70_000, "walk"), (9000, 5, "signed")]:
+        A = _values(r, n, vk)
+        Q = _queries(r, n, q, "uniform")
+        eps = np.empty(2 * q, ENDPOINT_DTYPE)
+        orc.port().orc_collect_endpoints(orc._p(Q), q, orc._p(eps))
+        orc.port().orc_sort_endpoints(orc._p(eps), 2 * q, 0)
+        con = engine.build_contracted(A, eps)
+        m = 2 * q
+        aqv = np.empty(m, np.int32)
+        aqo = np.empty(m, np.uint64)
+        bnd = np.empty(m, np.uint64)
+        import ctypes as C
+        nb = C.c_uint64()
+        orc.port().orc_build_contracted(orc._p(A), n, orc._p(eps), m, 1, orc._p(aqv), orc._p(aqo),
+                                        orc._p(bnd), C.byref(nb), None)
+        nbv = nb.value
+        assert np.array_equal(con.boundary, bnd[:nbv])
+        assert np.array_equal(con.aq_values, aqv[:max(nbv - 1, 0)])
+        assert np.array_equal(con.aq_origin, aqo[:max(nbv - 1, 0)])
+        cq = engine.remap_queries_from_sorted(eps, con, q)
+        cl = np.empty(q, np.uint32)
+        cr = np.empty(q, np.uint32)
+        dg = np.empty(q, np.uint8)
+        orc.port().orc_remap_from_sorted(orc._p(eps), m, orc._p(bnd), nbv, q, orc._p(cl), orc._p(cr),
+                                         orc._p(dg))
+        assert np.array_equal(cq.cleft, cl)
+        assert np.array_equal(cq.cright, cr)
+        assert np.array_equal(cq.degenerate, dg.astype(bool))
+
+
+def test_stage_contract_errors(engine):
+    A = np.arange(10, dtype=np.int32)
+    e = np.zeros(2, ENDPOINT_DTYPE)
+    e["pos"] = [5, 3]  # unsorted -> invalid_argument (contraction.cpp:123)
+    with pytest.raises(InvalidArgument):
+        engine.build_contracted(A, e)
+    # the bitmap was cleared: a valid call afterwards is exact
+    e["pos"] = [3, 5]
+    con = engine.build_contracted(A, e)
+    assert list(con.boundary) == [3, 5] and list(con.aq_origin) == [3]
+    # endpoint missing from boundary -> logic_error (contraction.cpp:182-183)
+    from paper_1706_06940_b200 import ContractedArray
+    bad = ContractedArray(np.zeros(0, np.int32), np.zeros(0, np.uint64), np.array([3], np.uint64))
+    with pytest.raises(LogicError):
+        engine.remap_queries_from_sorted(e, bad, 1)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 32, 512])
+def test_stage_block_sparse(engine, orc, k):
+    import ctypes as C
+    r = np.random.default_rng(k)
+    for m in (1, 2, 5, 1000, 100_000):
+        v = _values(r, m, "ties16")
+        table, b, levels = engine.build_block_sparse(v, k)
+        ref = np.empty(max(levels * b, 1), np.uint64)
+        bb, ll = C.c_uint64(), C.c_uint32()
+        orc.port().orc_build_block_sparse(orc._p(v), m, k, orc._p(ref), C.byref(bb), C.byref(ll))
+        assert (b, levels) == (bb.value, ll.value)
+        assert np.array_equal(table.reshape(-1), ref[: levels * b])
+    # values=[2,2,6], k=2 -> level0 [0,2], (1,0) = 0
+    t, b, lv = engine.build_block_sparse(np.array([2, 2, 6], np.int32), 2)
+    assert (b, lv) == (2, 2) and list(t[0]) == [0, 2] and t[1][0] == 0
+
+
+# ------------------------------------------------------------------ BASELINE configs
+from conftest import ROOT  # noqa: E402
+
+CONFIGS = {
+    # name: (array kind, n, query kind, q, seed offset)
+    "c1": (0, 1 << 20, 0, 1000, 1),
+    "c2": (0, 100_000_000, 0, 100_000, 2),
+    "c3": (0, 100_000_000, 1, 10_000_000, 3),
+    "c4": (1, 1_000_000_000, 2, 1_000_000, 4),
+    "c5": (2, 1 << 30, 0, 10_000_000, 5),
+}
+
+
+def _workload(name, n=None, q=None):
+    import ctypes as C
+    from paper_1706_06940_b200 import _lib
+    ak, n0, qk, q0, c = CONFIGS[name]
+    n = n or n0
+    q = q or q0
+    L = _lib.lib()
+    A = np.empty(n, np.int32)
+    Q = np.empty((q, 2), np.uint64)
+    assert L.brmq_workload_array(ak, n, 1706069400 + c, A.ctypes.data, 0) == 0
+    assert L.brmq_workload_queries(qk, n, q, 1706069400 + c, Q.ctypes.data, 0) == 0
+    return A, Q
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_configs_reduced(engine, orc, name):
+    """Every config's generators and variants at sizes the oracle finishes in seconds."""
+    sizes = {"c1": (None, None), "c2": (2_000_000, 20_000), "c3": (2_000_000, 400_000),
+             "c4": (4_000_000, 100_000), "c5": (1 << 22, 400_000)}
+    A, Q = _workload(name, *sizes[name])
+    want = orc.solve_oracle(A, Q)
+    for variant in VARIANTS:
+        got = _solve(engine, variant, A, Q, 512)
+        assert np.array_equal(got, want), (name, variant, np.nonzero(got != want)[0][:5])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_configs_full(engine, orc, name):
+    """BASELINE.json full sizes: bit-exact against the reference pipeline
+    (collect -> radix sort -> build_contracted -> ElementSparseTable), plus
+    size-independent properties (range membership, value = A[answer])."""
+    A, Q = _workload(name)
+    want = orc.solve_oracle(A, Q)
+    for variant in VARIANTS:
+        got = _solve(engine, variant, A, Q, 512)
+        assert np.array_equal(got, want), (name, variant, np.nonzero(got != want)[0][:5])
+    assert ((got >= Q[:, 0]) & (got <= Q[:, 1])).all()
