@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the batched-RMQ hot path on B200 (one JSON line on rank 0).
+
+Headline workload (BASELINE.json configs[1], "c2"): n = 1e8 int32 values uniform in
+[0, 2^31), q = 1e5 queries with uniform endpoints, BbST_CON (endpoint sort +
+segmented-argmin contraction + block Sparse Table over A_Q, k = 512).  One step =
+one complete batched solve (preprocessing included) with A and the queries
+resident in HBM; the L2 is flushed (256 MiB write) before every step, outside
+the per-step CUDA-event window.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--config c2] [--variant con_radix|con_bitmap|bbst] [--no-sweep]
+
+N > 1 (torchrun): every rank solves its own replica of the workload on its own
+GPU (the path does not shard on one node here: "replicas", weak scaling), the
+step time is the max over ranks, value = N*q / time.
+
+``--impl reference`` times the reference's own CPU pipeline (oracle/_ref, the
+reference sources compiled unmodified: collect -> radix sort ->
+build_contracted(threads = all cores) -> remap -> ElementSparseTable -> arg_min)
+on the same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (array kind, n, query kind, q, seed offset, default variant, description)
+    "c1": (0, 1 << 20, 0, 1000, 1, "con_radix", "n=2^20 uniform [0,2^31), q=1e3 uniform endpoints"),
+    "c2": (0, 100_000_000, 0, 100_000, 2, "con_radix",
+           "n=1e8 int32 uniform [0,2^31), q=1e5 uniform endpoints, BbST_CON k=512"),
+    "c3": (0, 100_000_000, 1, 10_000_000, 3, "bbst",
+           "n=1e8 uniform [0,2^31), q=1e7 log-uniform lengths, BbST (no contraction) k=512"),
+    "c4": (1, 1_000_000_000, 2, 1_000_000, 4, "bbst",
+           "n=1e9 values in [0,16), q=1e6 half short [1,256] half long, k=512"),
+    "c5": (2, 1 << 30, 0, 10_000_000, 5, "bbst",
+           "n=2^30 +-1 random walk, q=1e7 uniform endpoints, k=512"),
+}
+VARIANT_SORT = {"con_radix": 0, "con_bitmap": 2}
+SEED0 = 1706069400
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+def gen_workload(name: str, n: int | None = None, q: int | None = None):
+    from paper_1706_06940_b200 import _lib
+    ak, n0, qk, q0, c, _, _ = CONFIGS[name]
+    n, q = n or n0, q or q0
+    L = _lib.lib()
+    A = np.empty(n, np.int32)
+    Q = np.empty((q, 2), np.uint64)
+    assert L.brmq_workload_array(ak, n, SEED0 + c, A.ctypes.data, 0) == 0
+    assert L.brmq_workload_queries(qk, n, q, SEED0 + c, Q.ctypes.data, 0) == 0
+    return A, Q
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out = self.p.communicate(timeout=5)[0]
+            except Exception:
+                self.p.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args) -> dict:
+    import oracle
+    name = args.config
+    A, Q = gen_workload(name)
+    q = Q.shape[0]
+    th = oracle.nthreads()
+    L = oracle.ref()
+    out = np.empty(q, np.uint64)
+    stage = (C.c_double * 5)()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rc = L.ref_solve_oracle(A.ctypes.data, A.shape[0], Q.ctypes.data, q, th, out.ctypes.data, stage)
+        dt = time.perf_counter() - t0
+        assert rc == 0, rc
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    v = q / t
+    return {
+        "impl": "reference", "metric": metric_name(), "value": v, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": config_dict(name, "reference_cpu"),
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": th, "kind": "reference",
+                         "sample": f"full {name} workload per step (reference sources compiled "
+                                   f"unmodified, build_contracted threads={th})",
+                         "stage_ms_last": [x * 1e3 for x in stage]},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def metric_name() -> str:
+    return "batched RMQ queries/s incl. preprocess (n=1e8 int32); scan GB/s vs HBM peak"
+
+
+def config_dict(name: str, variant: str) -> dict:
+    ak, n, qk, q, c, _, desc = CONFIGS[name]
+    return {"workload": f"{name}: {desc}", "n": n, "q": q, "k": 512, "variant": variant,
+            "seed": SEED0 + c, "l2": "flushed before every step (256 MiB write, outside the timed window)",
+            "parallelism": "replicas (one independent solve per GPU)"}
+
+
+# ------------------------------------------------------------------ our arm
+def cpu_baseline(A, Q, name) -> dict:
+    import oracle
+    th = oracle.nthreads()
+    out = np.empty(Q.shape[0], np.uint64)
+    ts = []
+    budget = time.perf_counter() + 20.0
+    for _ in range(5):
+        t0 = time.perf_counter()
+        rc = oracle.ref().ref_solve_oracle(A.ctypes.data, A.shape[0], Q.ctypes.data, Q.shape[0], th,
+                                           out.ctypes.data, None)
+        ts.append(time.perf_counter() - t0)
+        assert rc == 0
+        if time.perf_counter() > budget:
+            break
+    t = statistics.median(ts)
+    return {"value": Q.shape[0] / t, "unit": "queries/s", "cores": th, "kind": "reference",
+            "sample": f"full {name} workload (n={A.shape[0]}, q={Q.shape[0]}), median of {len(ts)}, "
+                      "reference sources compiled unmodified (oracle/_ref)"}, out
+
+
+def time_solves(eng, torch, stream, fn, steps, warmup, flush):
+    """Per-step CUDA-event windows on the library stream; L2 flushed between steps."""
+    for _ in range(warmup):
+        flush.fill_(1)
+        fn()
+    torch.cuda.synchronize()
+    ms, stage_acc, launches = [], {}, 0
+    for _ in range(steps):
+        flush.fill_(1)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        fn()
+        e.record(stream)
+        e.synchronize()
+        ms.append(s.elapsed_time(e))
+        for nm, t, nl in eng.stage_times():
+            a = stage_acc.setdefault(nm, [0.0, 0])
+            a[0] += t
+            a[1] += nl
+        launches += eng.solve_info()["kernel_launches"]
+    return ms, {k: (v[0] / steps, v[1] // steps) for k, v in stage_acc.items()}, launches
+
+
+def run_ours(args) -> dict:
+    import torch
+    from paper_1706_06940_b200 import Engine, _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    name = args.config
+    variant = args.variant or CONFIGS[name][5]
+    A, Q = gen_workload(name)
+    n, q = A.shape[0], Q.shape[0]
+    eng = Engine(local)
+    # one explicit (non-default) stream shared by torch and the library, so the
+    # CUDA events, the L2 flush and the kernels are ordered on the same queue
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    eng.set_timing(True)
+    dA = torch.from_numpy(A).to(dev)
+    dQ = torch.from_numpy(Q.view(np.int64)).to(dev)
+    dAns = torch.empty(q, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def solve(a=dA, qq=dQ, out=dAns, v=variant):
+        if v == "bbst":
+            eng.solve_batch_bbst(a, qq, 512, out=out)
+        else:
+            eng.solve_batch_bbst_con(a, qq, 512, VARIANT_SORT[v], out=out)
+
+    # correctness gate on the bench workload itself (oracle on rank 0 host cores)
+    base, want = (None, None)
+    if rank == 0 and not args.no_cpu:
+        base, want = cpu_baseline(A, Q, name)
+    solve()
+    torch.cuda.synchronize()
+    if want is not None:
+        got = dAns.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), "bench answers differ from the reference oracle"
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ms, stages, launches = time_solves(eng, torch, stream, solve, args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    t_step = statistics.mean(ms)
+    if dist:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+        dist.barrier()
+    info = eng.solve_info()
+
+    # e2e: the public C-ABI with pinned HOST buffers, copies inside the window
+    L = _lib.lib()
+    hp = C.c_void_p()
+    nbytes_a, nbytes_q, nbytes_o = n * 4, q * 16, q * 8
+    assert L.brmq_host_alloc(C.byref(hp), nbytes_a + nbytes_q + nbytes_o) == 0
+    base_ptr = hp.value
+    C.memmove(base_ptr, A.ctypes.data, nbytes_a)
+    C.memmove(base_ptr + nbytes_a, Q.ctypes.data, nbytes_q)
+    hA = np.ctypeslib.as_array((C.c_int32 * n).from_address(base_ptr))
+    hQ = np.ctypeslib.as_array((C.c_uint64 * (2 * q)).from_address(base_ptr + nbytes_a)).reshape(q, 2)
+    hO = np.ctypeslib.as_array((C.c_uint64 * q).from_address(base_ptr + nbytes_a + nbytes_q))
+
+    def solve_host():
+        if variant == "bbst":
+            eng.solve_batch_bbst(hA, hQ, 512, out=hO)
+        else:
+            eng.solve_batch_bbst_con(hA, hQ, 512, VARIANT_SORT[variant], out=hO)
+
+    e2e_ms, _, _ = time_solves(eng, torch, stream, solve_host, max(3, args.steps // 2), 2, flush)
+    e2e_t = statistics.mean(e2e_ms)
+    if want is not None:
+        assert np.array_equal(hO, want), "e2e answers differ from the reference oracle"
+    L.brmq_host_free(hp)
+    if dist:
+        tt = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+
+    # roofline of the dominant kernel
+    pk = peaks()
+    dom = max(stages.items(), key=lambda kv: kv[1][0])[0]
+    if variant == "bbst":
+        alg_bytes = 4 * n  # block_argmin reads A once
+        dom_for_roof = "block_argmin"
+    else:
+        span = info["span_hi"] - info["span_lo"] + 1
+        aq = max(info["boundary"] - 1, 0)
+        alg_bytes = 4 * span + 8 * aq  # A span read + packed A_Q written
+        dom_for_roof = "contract"
+    kt = stages.get(dom_for_roof, (float("nan"), 0))[0]
+    achieved = alg_bytes / (kt * 1e-3) / 1e9 if kt > 0 else None
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(f"{name}/{variant}/{dom_for_roof}")
+    pre_ms = sum(v[0] for k, v in stages.items() if k not in ("query", "h2d", "d2h"))
+    pre_bytes = 4 * n if variant == "bbst" else 4 * (info["span_hi"] - info["span_lo"] + 1) + 16 * q + 8 * max(info["boundary"] - 1, 0)
+
+    rec = {
+        "metric": metric_name(), "value": world * q / (t_step * 1e-3), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": config_dict(name, variant),
+        "e2e": {"value": world * q / (e2e_t * 1e-3), "unit": "queries/s",
+                "h2d_bytes_per_step": nbytes_a + nbytes_q, "d2h_bytes_per_step": nbytes_o,
+                "ms_per_step": e2e_t},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom_for_roof, "achieved": achieved,
+                     "peak": pk["hbm_gbs"], "peak_src": pk["src"], "unit": "GB/s",
+                     "frac": (achieved / pk["hbm_gbs"]) if achieved else None,
+                     "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": kt},
+        "preprocess": {"ms": pre_ms, "alg_bytes": pre_bytes,
+                       "gbs": pre_bytes / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None},
+        "stages_ms": {k: round(v[0], 5) for k, v in stages.items()},
+        "dominant_stage": dom,
+        "clocks": clk.summary(),
+        "info": info,
+    }
+    if base is not None:
+        rec["cpu_baseline"] = base
+    if rank == 0 and args.sweep and world == 1:
+        rec["sweep"] = run_sweep(eng, torch, stream, flush, dA, A, args)
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+    return rec if rank == 0 else None
+
+
+def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
+    """North-star sweep: end-to-end queries/s at n = 1e8 for q = 1e3 .. 1e7, both variants
+    (device-resident inputs; each point checked against the oracle where cheap)."""
+    from paper_1706_06940_b200 import _lib
+    L = _lib.lib()
+    n = A.shape[0]
+    out = []
+    for q in (1_000, 10_000, 100_000, 1_000_000, 10_000_000):
+        Q = np.empty((q, 2), np.uint64)
+        L.brmq_workload_queries(0, n, q, SEED0 + 2, Q.ctypes.data, 0)
+        dQ = torch.from_numpy(Q.view(np.int64)).to(dA.device)
+        dO = torch.empty(q, dtype=torch.int64, device=dA.device)
+        for v in ("con_radix", "con_bitmap", "bbst"):
+            def f(v=v):
+                if v == "bbst":
+                    eng.solve_batch_bbst(dA, dQ, 512, out=dO)
+                else:
+                    eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[v], out=dO)
+            ms, stages, _ = time_solves(eng, torch, stream, f, 5, 2, flush)
+            t = statistics.mean(ms)
+            out.append({"q": q, "variant": v, "queries_per_s": q / (t * 1e-3), "ms": t,
+                        "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}})
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--variant", choices=["con_radix", "con_bitmap", "bbst"], default=None)
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / oracle gate")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        print(json.dumps(run_reference(args)))
+        return
+    rec = run_ours(args)
+    if rec is not None:
+        print(json.dumps(rec))
+
+
+if __name__ == "__main__":
+    main()

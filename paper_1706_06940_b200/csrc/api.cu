@@ -58,6 +58,8 @@ struct brmq_ctx {
     cudaStream_t stream = nullptr;
     char* ws = nullptr;  // grow-only workspace (zeroed on growth)
     size_t ws_cap = 0;
+    char* st = nullptr;  // grow-only arena that only ever holds epoch-tagged status words
+    size_t st_cap = 0;   // (so stale bytes can never alias a live epoch); zeroed on growth
     uint32_t* bitmap = nullptr;  // persistent, kept all-zero by the contraction kernel
     size_t bitmap_words = 0;
     Control* ctl_host = nullptr;  // pinned mirror of the control block
@@ -93,8 +95,21 @@ int ensure_ws(brmq_ctx* c, size_t bytes) {
     c->ws_cap = 0;
     size_t cap = align_up(bytes + bytes / 8, 1 << 21);
     CUDA_TRY(cudaMalloc(&c->ws, cap));
-    CUDA_TRY(cudaMemsetAsync(c->ws, 0, cap, c->stream));  // status words start invalid
+    CUDA_TRY(cudaMemsetAsync(c->ws, 0, cap, c->stream));
     c->ws_cap = cap;
+    return BRMQ_OK;
+}
+
+int ensure_status(brmq_ctx* c, size_t bytes) {
+    if (bytes <= c->st_cap) return BRMQ_OK;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->st) cudaFree(c->st);
+    c->st = nullptr;
+    c->st_cap = 0;
+    const size_t cap = align_up(bytes + bytes / 8, 1 << 20);
+    CUDA_TRY(cudaMalloc(&c->st, cap));
+    CUDA_TRY(cudaMemsetAsync(c->st, 0, cap, c->stream));
+    c->st_cap = cap;
     return BRMQ_OK;
 }
 
@@ -114,8 +129,8 @@ int ensure_bitmap(brmq_ctx* c, uint64_t n) {
 // Reserve `count` consecutive 24-bit epochs for single-pass scans.
 uint32_t take_epochs(brmq_ctx* c, uint32_t count) {
     if (c->epoch + count >= (1u << 24)) {
-        // wrap: every status word in the workspace is reset to "invalid"
-        cudaMemsetAsync(c->ws, 0, c->ws_cap, c->stream);
+        // wrap: every status word is reset to "invalid"
+        if (c->st) cudaMemsetAsync(c->st, 0, c->st_cap, c->stream);
         c->epoch = 1;
     }
     const uint32_t e = c->epoch;
@@ -230,6 +245,7 @@ void brmq_ctx_destroy(brmq_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& x : c->ev) cudaEventDestroy(x);
     if (c->ws) cudaFree(c->ws);
+    if (c->st) cudaFree(c->st);
     if (c->bitmap) cudaFree(c->bitmap);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->own) cudaStreamDestroy(c->own);
@@ -396,10 +412,11 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const size_t i_cr = cv.add(q * 4);
     const size_t i_aq = cv.add((aq_max + 2) * 8);
     const size_t i_st = cv.add(size_t(L) * b_max * 8);
-    const size_t i_cst = cv.add(ntiles * 8);
+    Carve sv;  // status arena
+    const size_t i_cst = sv.add(ntiles * 8);
     const size_t i_kag = cv.add(ntiles * 8);
     const size_t i_kin = cv.add(ntiles * 8);
-    size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_ust = 0, i_wi = 0;
+    size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_rst = 0, i_ust = 0, i_wi = 0;
     if (use_bitmap) {
         i_wi = cv.add((n / 32 + 2) * 8);
     } else {
@@ -408,19 +425,22 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         i_k1 = cv.add(m * 4);
         i_v1 = cv.add(m * 4);
         i_rs = cv.add(brmq::radix_sort_temp_bytes(m, bits));
-        i_ust = cv.add(brmq::unique_status_words(m) * 8);
+        i_rst = sv.add(brmq::radix_sort_status_words(m, bits) * 8);
+        i_ust = sv.add(brmq::unique_status_words(m) * 8);
     }
     const size_t i_a = dev ? 0 : cv.add(n * 4);
     const size_t i_q = dev ? 0 : cv.add(q * 16);
     const size_t i_ans = dev ? 0 : cv.add(q * 8);
     if (int rc = ensure_ws(c, cv.total)) return rc;
+    if (int rc = ensure_status(c, sv.total)) return rc;
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto S = [&](size_t i) { return reinterpret_cast<uint64_t*>(c->st + sv.off[i]); };
     auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
     auto* cl = reinterpret_cast<uint32_t*>(P(i_cl));
     auto* cr = reinterpret_cast<uint32_t*>(P(i_cr));
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
-    auto* cst = reinterpret_cast<uint64_t*>(P(i_cst));
+    auto* cst = S(i_cst);
     auto* kag = reinterpret_cast<uint64_t*>(P(i_kag));
     auto* kin = reinterpret_cast<uint64_t*>(P(i_kin));
     const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
@@ -454,14 +474,13 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         tm.stage("radix_sort", launches);
         bool in_alt = false;
         const uint32_t ep = take_epochs(c, uint32_t(brmq::radix_sort_passes(bits)));
-        l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), s, &in_alt, ep);
+        l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), S(i_rst), s, &in_alt, ep);
         launches += l;
         tm.end(l);
         tm.stage("unique_rank", launches);
         const uint32_t ep_u = take_epochs(c, 1);
         l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr, c->bitmap,
-                                ctl->span, &ctl->nb, &ctl->err,
-                                reinterpret_cast<uint64_t*>(P(i_ust)), &ctl->tickets[0], ep_u, s);
+                                ctl->span, &ctl->nb, &ctl->err, S(i_ust), &ctl->tickets[0], ep_u, s);
         launches += l;
         tm.end(l);
     }
@@ -550,6 +569,7 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
     const size_t i_rs = cv.add(brmq::radix_sort_temp_bytes(m, 32));
     const size_t i_e = dev ? 0 : cv.add(m * 8);
     if (int rc = ensure_ws(c, cv.total)) return rc;
+    if (int rc = ensure_status(c, brmq::radix_sort_status_words(m, 32) * 8)) return rc;
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
     cudaStream_t s = c->stream;
     void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
@@ -561,7 +581,8 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
     brmq::launch_split_eps(dE, m, k0, v0, s);
     bool in_alt = false;
     const uint32_t ep = take_epochs(c, 4);
-    brmq::launch_radix_sort(k0, v0, k1, v1, m, 32, P(i_rs), s, &in_alt, ep);
+    brmq::launch_radix_sort(k0, v0, k1, v1, m, 32, P(i_rs), reinterpret_cast<uint64_t*>(c->st), s,
+                            &in_alt, ep);
     brmq::launch_join_eps(in_alt ? k1 : k0, in_alt ? v1 : v0, m, dE, s);
     if (int rc = check_status(c)) return rc;
     if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));
@@ -585,15 +606,19 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     const size_t i_ctl = cv.add(sizeof(Control));
     const size_t i_k = cv.add(m * 4), i_v = cv.add(m * 4), i_bd = cv.add(m * 4);
     const size_t i_aq = cv.add((m + 2) * 8);
-    const size_t i_ust = cv.add(brmq::unique_status_words(m) * 8);
-    const size_t i_cst = cv.add(ntiles * 8), i_kag = cv.add(ntiles * 8), i_kin = cv.add(ntiles * 8);
+    Carve sv;
+    const size_t i_ust = sv.add(brmq::unique_status_words(m) * 8);
+    const size_t i_cst = sv.add(ntiles * 8);
+    const size_t i_kag = cv.add(ntiles * 8), i_kin = cv.add(ntiles * 8);
     const size_t i_a = dev ? 0 : cv.add(n * 4);
     const size_t i_e = dev ? 0 : cv.add(m * 8);
     const size_t i_av = dev ? 0 : cv.add(m * 4);
     const size_t i_ao = dev ? 0 : cv.add(m * 8);
     const size_t i_bo = dev ? 0 : cv.add(m * 8);
     if (int rc = ensure_ws(c, cv.total)) return rc;
+    if (int rc = ensure_status(c, sv.total)) return rc;
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto S = [&](size_t i) { return reinterpret_cast<uint64_t*>(c->st + sv.off[i]); };
     cudaStream_t s = c->stream;
     auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
     const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
@@ -613,7 +638,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     brmq::launch_split_eps(dE, m, k, v, s);
     const uint32_t ep_u = take_epochs(c, 1), ep_c = take_epochs(c, 1);
     brmq::launch_unique(k, v, m, n, bd, nullptr, nullptr, c->bitmap, ctl->span, &ctl->nb, &ctl->err,
-                        reinterpret_cast<uint64_t*>(P(i_ust)), &ctl->tickets[0], ep_u, s);
+                        S(i_ust), &ctl->tickets[0], ep_u, s);
     if (int rc = sync_and_read_control(c, ctl)) return rc;
     if (c->ctl_host->err) {
         // unsorted or out-of-range endpoints: clear any marks and report
@@ -621,7 +646,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         CUDA_TRY(cudaStreamSynchronize(s));
         return map_err(c->ctl_host->err);
     }
-    brmq::launch_contract(dA, n, c->bitmap, ctl->span, reinterpret_cast<uint64_t*>(P(i_cst)),
+    brmq::launch_contract(dA, n, c->bitmap, ctl->span, S(i_cst),
                           reinterpret_cast<uint64_t*>(P(i_kag)), reinterpret_cast<uint64_t*>(P(i_kin)),
                           &ctl->tickets[1], ep_c, AQ, &ctl->aq_len, &ctl->nb, nullptr, s);
     brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);

@@ -35,14 +35,15 @@ int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint
                             uint64_t* answers, cudaStream_t stream);
 
 // ---------------------------------------------------------------- radix_sort.cu
-size_t radix_sort_temp_bytes(uint64_t m, int bits);
+size_t radix_sort_temp_bytes(uint64_t m, int bits);     // zeroed scratch (histograms, tickets)
+size_t radix_sort_status_words(uint64_t m, int bits);   // epoch-tagged look-back words
 int radix_sort_passes(int bits);
 // Stable LSD sort of (key, value) u32 pairs by the low `bits` key bits; uses
 // epochs epoch_base .. epoch_base + passes - 1.  *result_in_alt tells whether
 // the sorted data ended in alt_keys / alt_vals.
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
-                      uint64_t m, int bits, void* tmp, cudaStream_t stream, bool* result_in_alt,
-                      uint32_t epoch_base);
+                      uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
+                      bool* result_in_alt, uint32_t epoch_base);
 
 // ---------------------------------------------------------------- contract.cu
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,

@@ -140,28 +140,26 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
 
 }  // namespace
 
-size_t radix_sort_temp_bytes(uint64_t m, int bits) {
-    const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
-    const uint64_t tiles = (m + kTile - 1) / kTile;
-    // [ghist: 4*256 u64][tickets: 4 u32 padded to 256 B][status: passes * tiles * 256 u64]
-    return size_t(kMaxPasses * kRadix * 8) + 256 + size_t(passes) * tiles * kRadix * 8;
-}
+// [ghist: 4*256 u64][tickets: 4 u32 padded to 256 B], zeroed by every sort
+size_t radix_sort_temp_bytes(uint64_t, int) { return size_t(kMaxPasses * kRadix * 8) + 256; }
 
-size_t radix_sort_zero_bytes() { return size_t(kMaxPasses * kRadix * 8) + 256; }
+size_t radix_sort_status_words(uint64_t m, int bits) {
+    const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
+    return size_t(passes) * ((m + kTile - 1) / kTile) * kRadix;
+}
 
 int radix_sort_passes(int bits) { return bits <= 0 ? 0 : (bits + 7) / 8; }
 
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
-                      uint64_t m, int bits, void* tmp, cudaStream_t stream, bool* result_in_alt,
-                      uint32_t epoch_base) {
+                      uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
+                      bool* result_in_alt, uint32_t epoch_base) {
     *result_in_alt = false;
     if (m <= 1 || bits <= 0) return 0;
     const int passes = (bits + 7) / 8;
     const uint64_t tiles = (m + kTile - 1) / kTile;
     auto* ghist = static_cast<unsigned long long*>(tmp);
     auto* tickets = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8);
-    auto* status = reinterpret_cast<uint64_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8 + 256);
-    cudaMemsetAsync(tmp, 0, radix_sort_zero_bytes(), stream);
+    cudaMemsetAsync(tmp, 0, radix_sort_temp_bytes(m, bits), stream);
     int launches = 0;
     {
         uint64_t blocks = (m + kThreads * 8 - 1) / (kThreads * 8);

@@ -284,3 +284,21 @@ def test_configs_full(engine, orc, name):
         got = _solve(engine, variant, A, Q, 512)
         assert np.array_equal(got, want), (name, variant, np.nonzero(got != want)[0][:5])
     assert ((got >= Q[:, 0]) & (got <= Q[:, 1])).all()
+
+
+def test_workspace_reuse_sequence(engine, orc):
+    """Solves of different shapes back to back on one context: the grow-only
+    workspace holds stale data from earlier calls, which must never be read as
+    live look-back status (regression: status words now live in their own arena)."""
+    r = np.random.default_rng(99)
+    n = 3_000_000
+    A = _values(r, n, "uniform")
+    Qbig = _queries(r, n, 300_000, "uniform")
+    assert np.array_equal(engine.solve_batch_bbst_con(A, Qbig, 512, SortKind.Radix),
+                          orc.solve_oracle(A, Qbig))
+    for q in (1_000, 100_000, 10, 250_000, 3_000, 600_000, 1):
+        Q = _queries(r, n, q, "uniform" if q % 2 else "mixed")
+        want = orc.solve_oracle(A, Q)
+        for variant in VARIANTS:
+            got = _solve(engine, variant, A, Q, 512)
+            assert np.array_equal(got, want), (q, variant, np.nonzero(got != want)[0][:5])
