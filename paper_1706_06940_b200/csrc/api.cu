@@ -114,7 +114,7 @@ int ensure_status(brmq_ctx* c, size_t bytes) {
 }
 
 int ensure_bitmap(brmq_ctx* c, uint64_t n) {
-    const size_t words = size_t(n / 32 + 2);
+    const size_t words = brmq::contract_bitmap_words(n);  // whole tiles
     if (words <= c->bitmap_words) return BRMQ_OK;
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->bitmap) cudaFree(c->bitmap);
@@ -413,9 +413,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const size_t i_aq = cv.add((aq_max + 2) * 8);
     const size_t i_st = cv.add(size_t(L) * b_max * 8);
     Carve sv;  // status arena
-    const size_t i_cst = sv.add(ntiles * 8);
-    const size_t i_kag = cv.add(ntiles * 8);
-    const size_t i_kin = cv.add(ntiles * 8);
+    const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
     size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_rst = 0, i_ust = 0, i_wi = 0;
     if (use_bitmap) {
         i_wi = cv.add((n / 32 + 2) * 8);
@@ -441,8 +439,6 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
     auto* cst = S(i_cst);
-    auto* kag = reinterpret_cast<uint64_t*>(P(i_kag));
-    auto* kin = reinterpret_cast<uint64_t*>(P(i_kin));
     const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
@@ -485,9 +481,9 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         tm.end(l);
     }
     tm.stage("contract", launches);
-    l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, cst, kag, kin, &ctl->tickets[1],
-                              ep_contract, AQ, &ctl->aq_len, &ctl->nb,
-                              use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, s);
+    l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len,
+                              use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
+                              ep_contract, s);
     launches += l;
     tm.end(l);
     if (use_bitmap) {
@@ -608,8 +604,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     const size_t i_aq = cv.add((m + 2) * 8);
     Carve sv;
     const size_t i_ust = sv.add(brmq::unique_status_words(m) * 8);
-    const size_t i_cst = sv.add(ntiles * 8);
-    const size_t i_kag = cv.add(ntiles * 8), i_kin = cv.add(ntiles * 8);
+    const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
     const size_t i_a = dev ? 0 : cv.add(n * 4);
     const size_t i_e = dev ? 0 : cv.add(m * 8);
     const size_t i_av = dev ? 0 : cv.add(m * 4);
@@ -646,9 +641,8 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         CUDA_TRY(cudaStreamSynchronize(s));
         return map_err(c->ctl_host->err);
     }
-    brmq::launch_contract(dA, n, c->bitmap, ctl->span, S(i_cst),
-                          reinterpret_cast<uint64_t*>(P(i_kag)), reinterpret_cast<uint64_t*>(P(i_kin)),
-                          &ctl->tickets[1], ep_c, AQ, &ctl->aq_len, &ctl->nb, nullptr, s);
+    brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len, nullptr,
+                          S(i_cst), ep_c, s);
     brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);
     brmq::launch_u32_to_u64(bd, &ctl->nb, m, dbo, s);
     if (int rc = check_status(c)) return rc;

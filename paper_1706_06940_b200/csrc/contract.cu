@@ -1,5 +1,6 @@
-// contract.cu -- BbST_CON stages 1-2 on the device: endpoints, dedup/rank,
-// and the segmented argmin that contracts A into A_Q.
+// contract.cu -- BbST_CON stage 1 on the device: endpoints, dedup/rank and the
+// boundary bitmap consumed by the contraction kernel (contraction.cu), plus
+// the bitmap remap and the stage-API helper kernels.
 //
 // Reference stages replaced:
 //   collect_endpoints          contraction.cpp:13-23
@@ -8,20 +9,9 @@
 //   remap_queries_from_sorted  contraction.cpp:174-199
 //
 // B200 design.  The boundary set is handed to the contraction kernel as a
-// bitmap over A (bit p set <=> p is a query endpoint), so a tile of A finds
-// its area boundaries with one coalesced 512-byte read instead of a search
-// in the sorted boundary list.  The contraction kernel is ONE streaming pass
-// over A[b_0 .. b_last]: each CTA owns a 4096-element tile (16 elements per
-// thread), computes per thread (boundary count, open-segment min), runs a
-// block-wide segmented-min + sum scan, publishes the tile aggregate and
-// resolves the segment that enters the tile from the left with a decoupled
-// look-back over epoch-tagged tile descriptors.  A second walk over the
-// registers then writes each finished area as a packed key (value, leftmost
-// A position), i.e. aq_values and aq_origin in one 8-byte word.  Area t is
-// closed with the boundary element A[b_{t+1}] that opens area t+1, which
-// restores the reference's inclusive-both-ends areas (contraction.hpp:25-27)
-// with every element read once.  The kernel clears the bitmap words it
-// consumed, so the bitmap never needs a memset.
+// bitmap over A (bit p set <=> p is a query endpoint), so a tile of A finds its
+// area boundaries with one coalesced read of its bitmap words instead of a
+// search in the sorted boundary list (see contraction.cu for the scan of A).
 //
 // Two ways to produce the bitmap + query ranks (BRMQ_SORT_* in brmq.h):
 //   radix  : k_collect -> device radix sort (radix_sort.cu) -> k_unique
@@ -42,15 +32,19 @@ constexpr int kTile = kThreads * kItems;  // 4096
 
 // ------------------------------------------------------------------ collect
 // span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
+// Grid-stride with a capped grid so the span needs only 2 atomics per CTA.
 __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restrict__ Q, uint64_t q,
                                                       uint64_t n, uint32_t* __restrict__ keys,
                                                       uint32_t* __restrict__ vals,
                                                       uint32_t* __restrict__ bitmap,
                                                       uint32_t* __restrict__ span,
                                                       uint32_t* __restrict__ err) {
-    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
-    uint32_t lo = 0xFFFFFFFFu, hi = 0;
-    if (i < q) {
+    __shared__ uint32_t s_lo, s_hi;
+    if (threadIdx.x == 0) { s_lo = 0xFFFFFFFFu; s_hi = 0; }
+    __syncthreads();
+    uint32_t lo_acc = 0xFFFFFFFFu, hi_acc = 0;
+    const uint64_t stride = uint64_t(gridDim.x) * kThreads;
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < q; i += stride) {
         const ulonglong2 x = __ldg(Q + i);
         uint64_t l = x.x, r = x.y;
         if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
@@ -59,8 +53,7 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
             r = n - 1;
             if (l > r) l = r;
         }
-        lo = uint32_t(l);
-        hi = uint32_t(r);
+        const uint32_t lo = uint32_t(l), hi = uint32_t(r);
         if (keys) {
             reinterpret_cast<uint2*>(keys)[i] = make_uint2(lo, hi);
             reinterpret_cast<uint2*>(vals)[i] =
@@ -70,13 +63,20 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
             atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
             atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
         }
+        lo_acc = lo < lo_acc ? lo : lo_acc;
+        hi_acc = hi > hi_acc ? hi : hi_acc;
     }
     if (span) {
-        const uint32_t wlo = __reduce_min_sync(kFull, lo);
-        const uint32_t whi = __reduce_max_sync(kFull, hi);
+        const uint32_t wlo = __reduce_min_sync(kFull, lo_acc);
+        const uint32_t whi = __reduce_max_sync(kFull, hi_acc);
         if (lane_id() == 0 && wlo != 0xFFFFFFFFu) {
-            atomicMax(span + 0, ~wlo);
-            atomicMax(span + 1, whi);
+            atomicMin(&s_lo, wlo);
+            atomicMax(&s_hi, whi);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_lo != 0xFFFFFFFFu) {
+            atomicMax(span + 0, ~s_lo);
+            atomicMax(span + 1, s_hi);
         }
     }
 }
@@ -126,15 +126,21 @@ __global__ void __launch_bounds__(kThreads) k_unique(
     if (unsorted) atomicOr(err, 4u);
     uint32_t total;
     const uint32_t excl = block_excl_sum<kThreads>(cnt, s_scan, total);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         if (tile == 0) {
-            st_relaxed_u64(status, status_pack(epoch, kStInclusive, false, total));
-            s_excl = 0;
+            if (threadIdx.x == 0) {
+                st_release_u64(status, status_pack(epoch, kStInclusive, false, total));
+                s_excl = 0;
+            }
         } else {
-            st_relaxed_u64(status + tile, status_pack(epoch, kStAggregate, false, total));
-            const uint64_t e = lookback_sum(status, tile, epoch);
-            st_relaxed_u64(status + tile, status_pack(epoch, kStInclusive, false, e + total));
-            s_excl = e;
+            if (threadIdx.x == 0)
+                st_release_u64(status + tile, status_pack(epoch, kStAggregate, false, total));
+            uint64_t e, unused;
+            warp_lookback<false>(status, nullptr, nullptr, tile, 0, epoch, e, unused);
+            if (threadIdx.x == 0) {
+                st_release_u64(status + tile, status_pack(epoch, kStInclusive, false, e + total));
+                s_excl = e;
+            }
         }
     }
     __syncthreads();
@@ -166,139 +172,6 @@ __global__ void __launch_bounds__(kThreads) k_unique(
             *nb_out = r;
             if (span) span[1] = p[j];
         }
-    }
-}
-
-// ----------------------------------------------------------------- contract
-__device__ __forceinline__ uint64_t wait_acquire(const uint64_t* status, uint64_t t, uint32_t epoch) {
-    uint64_t s;
-    while (true) {
-        s = ld_acquire_u64(status + t);
-        if (status_state(s, epoch) != kStInvalid) break;
-        __nanosleep(32);
-    }
-    return s;
-}
-
-__global__ void __launch_bounds__(kThreads) k_contract(
-    const int32_t* __restrict__ A, uint64_t n, uint32_t* __restrict__ bitmap,
-    const uint32_t* __restrict__ span, uint64_t* __restrict__ status, uint64_t* __restrict__ key_agg,
-    uint64_t* __restrict__ key_inc, uint32_t* __restrict__ ticket, uint32_t epoch,
-    uint64_t* __restrict__ aq, uint64_t* __restrict__ aq_len, uint64_t* __restrict__ nb_out,
-    uint2* __restrict__ word_info) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint64_t shk[kThreads / 32 + 1];
-    __shared__ uint32_t shf[kThreads / 32 + 1], shc[kThreads / 32 + 1];
-    __shared__ unsigned long long s_excl;
-    __shared__ uint64_t s_carry;
-
-    const uint32_t b0 = ~span[0], blast = span[1];
-    if (b0 > blast) return;  // no endpoints
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint64_t tfirst = b0 / kTile, tlast = blast / kTile;
-    const uint64_t t = tfirst + s_tile;
-    if (t > tlast) return;
-    const uint64_t p0 = t * kTile + uint64_t(threadIdx.x) * kItems;
-
-    // boundary flags for this thread's 16 positions (two threads share a word)
-    uint32_t word = 0;
-    if (p0 < n) word = bitmap[p0 >> 5];
-    const uint32_t fl = (word >> (p0 & 31)) & 0xFFFFu;
-
-    // the thread's 16 elements; positions outside [b0, blast] are not in any area
-    const bool any = p0 <= blast && p0 + kItems - 1 >= b0;
-    int32_t v[kItems];
-    if (any) {
-        if (p0 + kItems <= n && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
-            const int4* a4 = reinterpret_cast<const int4*>(A + p0);
-#pragma unroll
-            for (int j = 0; j < kItems / 4; ++j) {
-                const int4 x = __ldg(a4 + j);
-                v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kItems; ++j) v[j] = p0 + j < n ? __ldg(A + p0 + j) : 0;
-        }
-    }
-    // pass 1: count and the min of the segment open at the thread's right end
-    uint64_t run = kNoKey;
-    if (any) {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            const uint64_t p = p0 + j;
-            if (p < b0 || p > blast) continue;
-            const uint64_t key = pack_key(v[j], uint32_t(p));
-            run = ((fl >> j) & 1u) ? key : kmin(run, key);
-        }
-    }
-    const uint32_t cnt = __popc(fl);
-    SegMin xe, xt;
-    uint32_t ce, ct;
-    block_excl_segmin_sum<kThreads>(SegMin{run, cnt != 0}, cnt, xe, ce, xt, ct, shk, shf, shc);
-
-    // tile descriptor + decoupled look-back (thread 0)
-    if (threadIdx.x == 0) {
-        if (t == tfirst) {  // first tile starts with b0: nothing enters from the left
-            key_inc[t] = xt.k;
-            st_release_u64(status + t, status_pack(epoch, kStInclusive, xt.f, ct));
-            s_excl = 0;
-            s_carry = kNoKey;
-        } else {
-            key_agg[t] = xt.k;
-            st_release_u64(status + t, status_pack(epoch, kStAggregate, xt.f, ct));
-            uint64_t excl = 0, carry = kNoKey;
-            bool key_done = false;
-            uint64_t p = t;
-            while (p > tfirst) {
-                --p;
-                const uint64_t s = wait_acquire(status, p, epoch);
-                excl += status_value(s);
-                if (status_state(s, epoch) == kStInclusive) {
-                    if (!key_done) carry = kmin(carry, ld_relaxed_u64(key_inc + p));
-                    break;
-                }
-                if (!key_done) {
-                    carry = kmin(carry, ld_relaxed_u64(key_agg + p));
-                    key_done = status_flag(s);
-                }
-            }
-            key_inc[t] = xt.f ? xt.k : kmin(carry, xt.k);
-            st_release_u64(status + t, status_pack(epoch, kStInclusive, false, excl + ct));
-            s_excl = excl;
-            s_carry = carry;
-        }
-    }
-    __syncthreads();
-
-    // pass 2: write the areas closed inside this thread
-    uint64_t cur = xe.f ? xe.k : kmin(s_carry, xe.k);
-    uint64_t rank = s_excl + ce;  // boundaries strictly before p0
-    if (any) {
-#pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-            const uint64_t p = p0 + j;
-            if (p < b0 || p > blast) continue;
-            const uint64_t key = pack_key(v[j], uint32_t(p));
-            if ((fl >> j) & 1u) {
-                if (rank > 0) aq[rank - 1] = kmin(cur, key);  // close area rank-1 with A[b]
-                ++rank;
-                cur = key;                                     // b opens the next area
-            } else {
-                cur = kmin(cur, key);
-            }
-        }
-    }
-    // consumed bitmap words: hand out (prefix, bits) for the remap, then clear
-    if ((p0 & 31) == 0 && word != 0) {
-        if (word_info) word_info[p0 >> 5] = make_uint2(uint32_t(s_excl + ce), word);
-        bitmap[p0 >> 5] = 0;
-    }
-    if (t == tlast && threadIdx.x == 0) {
-        const uint64_t nb = s_excl + ct;
-        *nb_out = nb;
-        *aq_len = nb - 1;
     }
 }
 
@@ -389,7 +262,8 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s) {
     if (q == 0) return 0;
-    k_collect<<<g256(q), kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
+    const unsigned grid = g256(q) < 148u * 16u ? g256(q) : 148u * 16u;
+    k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
                                            bitmap, span, err);
     return 1;
 }
@@ -403,18 +277,6 @@ int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t
     if (m == 0) return 0;
     k_unique<<<unsigned((m + kTile - 1) / kTile), kThreads, 0, s>>>(
         pos, org, m, n, boundary, cleft, cright_raw, bitmap, span, nb_out, err, status, ticket, epoch);
-    return 1;
-}
-
-size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
-
-int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
-                    uint64_t* status, uint64_t* key_agg, uint64_t* key_inc, uint32_t* ticket,
-                    uint32_t epoch, uint64_t* aq, uint64_t* aq_len, uint64_t* nb_out,
-                    uint2* word_info, cudaStream_t s) {
-    if (n == 0) return 0;
-    k_contract<<<unsigned(contract_tiles(n)), kThreads, 0, s>>>(
-        A, n, bitmap, span, status, key_agg, key_inc, ticket, epoch, aq, aq_len, nb_out, word_info);
     return 1;
 }
 

@@ -53,11 +53,15 @@ int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
                   uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
                   uint32_t* ticket, uint32_t epoch, cudaStream_t s);
-size_t contract_tiles(uint64_t n);
+size_t contract_tiles(uint64_t n);  // 8192-element tiles over A
+size_t contract_bitmap_words(uint64_t n);  // bitmap words the contraction reads (whole tiles)
+size_t contract_status_words();    // status-arena words the contraction needs
+// Persistent cooperative contraction (contract.cu): bitmap of boundaries ->
+// packed A_Q keys, |boundary| (nb_out) and |A_Q|; word_info (nullable) gets
+// (rank prefix, bits) of every non-empty bitmap word, which is cleared.
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
-                    uint64_t* status, uint64_t* key_agg, uint64_t* key_inc, uint32_t* ticket,
-                    uint32_t epoch, uint64_t* aq, uint64_t* aq_len, uint64_t* nb_out,
-                    uint2* word_info, cudaStream_t s);
+                    uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
+                    uint64_t* status, uint32_t epoch, cudaStream_t s);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)

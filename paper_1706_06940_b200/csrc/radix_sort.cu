@@ -59,12 +59,15 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
                                                       uint32_t epoch) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t whist[kWarps][kRadix];
+    __shared__ uint32_t thist[kRadix];
     __shared__ unsigned long long s_base[kRadix];
     __shared__ uint32_t s_scan[kWarps + 1];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t d = threadIdx.x;  // the digit this thread publishes / looks back for
 
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
+    thist[d] = 0;
     __syncthreads();
     const uint64_t tile = s_tile;
     const uint64_t base = tile * kTile + uint64_t(warp) * (32 * kItems);
@@ -78,7 +81,17 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
         val[i] = ok ? __ldg(vin + idx) : 0u;
         dig[i] = ok ? ((key[i] >> shift) & 0xFFu) : 0x100u;  // 0x100 = no key
     }
-    // Stable warp-level ranking: item-major, lane-minor == input order.
+    // 1) tile digit histogram, published at once so successors never wait on
+    //    this tile's ranking work (decoupled look-back)
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+        if (dig[i] < 0x100u) atomicAdd(&thist[dig[i]], 1u);
+    __syncthreads();
+    const uint32_t tcount = thist[d];
+    uint64_t* st = status + tile * kRadix;
+    st_relaxed_u64(st + d, status_pack(epoch, tile == 0 ? kStInclusive : kStAggregate, false, tcount));
+
+    // 2) stable warp-level ranking: item-major, lane-minor == input order
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
@@ -94,8 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
     }
     __syncthreads();
 
-    // Thread d owns digit d: warp offsets, tile count, look-back, global base.
-    const uint32_t d = threadIdx.x;
+    // 3) per digit: warp offsets, global digit base, look-back over tiles
     uint32_t sum = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
@@ -103,27 +115,22 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
         whist[w][d] = sum;
         sum += c;
     }
-    uint64_t* st = status + tile * kRadix;
-    if (tile == 0) {
-        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, sum));
-    } else {
-        st_relaxed_u64(st + d, status_pack(epoch, kStAggregate, false, sum));
-    }
-    // Global exclusive digit offsets from the histogram (block scan of 256 counts).
-    const unsigned long long g = ghist[d];
-    // 64-bit exclusive scan via two 32-bit halves is overkill: counts <= 2^32.
     uint32_t gtot;
-    const uint32_t gex = block_excl_sum<kThreads>(uint32_t(g), s_scan, gtot);
+    const uint32_t gex = block_excl_sum<kThreads>(uint32_t(ghist[d]), s_scan, gtot);
     uint64_t excl = 0;
     if (tile > 0) {
         uint64_t p = tile;
         while (p > 0) {
             --p;
-            const uint64_t s = status_wait(status + p * kRadix, d, epoch);
-            excl += status_value(s);
-            if (status_state(s, epoch) == kStInclusive) break;
+            uint64_t sw;
+            while (true) {
+                sw = ld_relaxed_u64(status + p * kRadix + d);
+                if (status_state(sw, epoch) != kStInvalid) break;
+            }
+            excl += status_value(sw);
+            if (status_state(sw, epoch) == kStInclusive) break;
         }
-        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, excl + sum));
+        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, excl + tcount));
     }
     s_base[d] = (unsigned long long)gex + excl;
     __syncthreads();

@@ -56,6 +56,64 @@ __device__ __forceinline__ uint64_t lookback_sum(const uint64_t* status, uint64_
     return excl;
 }
 
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// Warp-wide decoupled look-back (call with all 32 lanes of one warp).
+// Reads the descriptors of 32 predecessors per round (lane i <- tile p - i),
+// waits only until every lane up to the nearest inclusive ("P") one is
+// published, and folds them: `excl` = sum of the values up to that tile;
+// with KEYS, `carry` = min of the keys of the open segment entering `tile`
+// (aggregate keys until the nearest tile holding a segment head, whose
+// aggregate is its tail, or the nearest P tile, whose inclusive key is the
+// open-segment min at its end).  Tiles before `tfirst` do not exist.
+template <bool KEYS>
+__device__ __forceinline__ void warp_lookback(const uint64_t* status, const uint64_t* key_agg,
+                                              const uint64_t* key_inc, uint64_t tile,
+                                              uint64_t tfirst, uint32_t epoch, uint64_t& excl,
+                                              uint64_t& carry) {
+    const unsigned lane = lane_id();
+    excl = 0;
+    carry = kNoKey;
+    bool key_done = false;
+    int64_t p = int64_t(tile) - 1;
+    while (true) {
+        const int64_t ti = p - int64_t(lane);
+        const bool exists = ti >= int64_t(tfirst);
+        uint64_t s = 0, st = kStInclusive;
+        while (true) {
+            if (exists) {
+                s = ld_acquire_u64(status + ti);
+                st = status_state(s, epoch);
+            }
+            const unsigned inv = __ballot_sync(kFull, st == kStInvalid);
+            const unsigned pm = __ballot_sync(kFull, st == kStInclusive);
+            const int lowp = pm ? __ffs(pm) - 1 : 31;
+            const unsigned upto = lowp >= 31 ? kFull : ((2u << lowp) - 1u);
+            if ((inv & upto) == 0) break;
+            __nanosleep(20);
+        }
+        const unsigned pm = __ballot_sync(kFull, st == kStInclusive);
+        const int g = pm ? __ffs(pm) - 1 : 32;  // nearest inclusive lane (32: none)
+        excl += warp_sum_u64((int(lane) <= g && exists) ? status_value(s) : 0);
+        if (KEYS && !key_done) {
+            const unsigned fm = __ballot_sync(kFull, st == kStAggregate && status_flag(s));
+            const int f = fm ? __ffs(fm) - 1 : 32;
+            const int stop = f < g ? f : g;
+            uint64_t kk = kNoKey;
+            if (int(lane) <= stop && exists)
+                kk = ld_relaxed_u64((st == kStInclusive ? key_inc : key_agg) + ti);
+            carry = kmin(carry, warp_min_key(kk));
+            key_done = stop < 32;
+        }
+        if (g < 32) break;
+        p -= 32;
+    }
+}
+
 // Block-wide exclusive sum (blockDim.x == NT, NT % 32 == 0).  `total` gets the
 // block total.  Uses NT/32 + 1 words of shared scratch.
 template <int NT>

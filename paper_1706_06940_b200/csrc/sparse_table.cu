@@ -11,8 +11,8 @@
 // "t" positions (column = r + s*t) plus a halo of 2^D - 1 t-positions,
 // doubles D times in shared memory (ping-pong buffers, one barrier per level)
 // and writes each finished level straight to its row.  base = 0 uses R = 1
-// (plain contiguous columns, D <= 10); higher bases use R = 32 residues so
-// every global access is a 256-byte contiguous run.  b = 2M (n = 2^30,
+// (plain contiguous columns, D <= 10); higher bases use R = 8 residues so
+// every global access is a 64-byte contiguous run.  b = 2M (n = 2^30,
 // k = 512, 22 levels) needs 3 launches instead of 21.
 #include "common.cuh"
 #include "kernels.h"
@@ -81,7 +81,7 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
     while (base < L - 1) {
         if (base == 0) {
             const uint32_t D = (L - 1) < 10 ? (L - 1) : 10;
-            const uint32_t T = 2048;
+            const uint32_t T = b >= 65536 ? 256 : 1024;  // >= 2-5 CTAs per SM on big tables
             const uint64_t tiles = (b + T - 1) / T;
             const size_t sm = size_t(2) * (T + (1u << D) - 1) * sizeof(uint64_t);
             cudaFuncSetAttribute(k_st_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -89,15 +89,15 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
             base = D;
         } else {
             const uint32_t D = (L - 1 - base) < 7 ? (L - 1 - base) : 7;
-            const uint32_t T = 64;
+            const uint32_t T = 32;
             const uint64_t s = 1ull << base;
-            const uint64_t groups = s / 32;  // base >= 10 here
+            const uint64_t groups = s / 8;  // base >= 10 here; 8 residues = 64-byte runs
             const uint64_t tcount = (b + s - 1) / s;
             const uint64_t tiles = (tcount + T - 1) / T;
-            const size_t sm = size_t(2) * (T + (1u << D) - 1) * 32 * sizeof(uint64_t);
-            cudaFuncSetAttribute(k_st_tile<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_st_tile<32><<<unsigned(groups * tiles), kThreads, sm, stream>>>(ST, b, b_dev, base, D, T,
-                                                                              groups);
+            const size_t sm = size_t(2) * (T + (1u << D) - 1) * 8 * sizeof(uint64_t);
+            cudaFuncSetAttribute(k_st_tile<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_st_tile<8><<<unsigned(groups * tiles), kThreads, sm, stream>>>(ST, b, b_dev, base, D, T,
+                                                                             groups);
             base += D;
         }
         ++launches;
