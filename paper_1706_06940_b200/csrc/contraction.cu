@@ -35,6 +35,7 @@
 // The kernel clears the bitmap words it consumed (the bitmap is never
 // memset) and, for the bitmap pipeline, emits (rank prefix, bits) of every
 // non-empty word for the query remap.
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -50,7 +51,7 @@ constexpr int NT = 128;             // threads per CTA
 constexpr int NW = NT / 32;         // warps per CTA
 constexpr int kRow = 32;            // positions per thread = one 128-byte row
 constexpr int kTile = NT * kRow;    // 4096 positions = 16 KB per tile
-constexpr int kStages = 4;          // TMA ring depth
+constexpr int kMaxStages = 4;       // TMA ring depth (runtime: ContractArgs::stages)
 constexpr int kDense = 4;           // flagged rows per warp above which rows close per thread
 
 struct __align__(1024) Stage {
@@ -178,6 +179,8 @@ struct ContractArgs {
     uint64_t* st_part;   // [G] epoch-tagged partial descriptors (phase C)
     uint64_t* key_tail;  // [G]
     uint32_t epoch;
+    uint32_t stages;  // TMA ring depth, 2..kMaxStages
+    uint32_t debug;   // profiling knob: 1 = stream only (no compute)
 };
 
 template <bool TMA>
@@ -188,6 +191,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
     const uint32_t sbase = (raw + 1023u) & ~1023u;  // 1024-byte aligned: 128-byte swizzle atoms
     unsigned char* base_ptr = smem_raw + (sbase - raw);
     Stage* stg = reinterpret_cast<Stage*>(base_ptr);
+    const uint32_t kStages = c.stages;
     uint32_t* sbits = reinterpret_cast<uint32_t*>(base_ptr + (TMA ? kStages * sizeof(Stage) : 0));
     uint64_t* bars = reinterpret_cast<uint64_t*>(sbits + (TMA ? kStages * NT : 0));
     __shared__ uint64_t s_tk[2][NW];  // double-buffered warp totals of the tile scan
@@ -210,27 +214,34 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
 
     auto issue = [&](uint64_t i) {  // thread 0: tile ta+i -> stage i % kStages
         const uint64_t t = ta + i;
-        const int st = int(i % kStages);
+        const uint32_t st = uint32_t(i % kStages);
         fence_proxy_async();
         mbar_arrive_expect_tx(&bars[st], uint32_t(sizeof(Stage)) + NT * 4u);
         tma_load_2d(stg[st].a, &tmap, 0, int(t * NT), &bars[st]);
         bulk_g2s(sbits + st * NT, c.bitmap + t * NT, NT * 4u, &bars[st]);
     };
     if (TMA && tid == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
+        for (uint32_t st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
         fence_mbar_init();
         for (uint64_t i = 0; i < my_count && i < uint64_t(kStages); ++i) issue(i);
     }
     if (tid == 0) s_head = kNoKey;
 
     // ---- A: boundaries in the range, published at once; base = sum of predecessors
-    {
+    if (c.debug == 2) {
+        if (tid == 0) s_base = 0;
+        __syncthreads();
+    } else {
         const uint4* w4 = reinterpret_cast<const uint4*>(c.bitmap + ta * NT);
         const uint64_t nvec = my_count * (NT / 4);
         uint32_t cnt = 0;
-        for (uint64_t j = tid; j < nvec; j += NT) {
-            const uint4 w = __ldg(w4 + j);
-            cnt += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+        for (uint64_t j0 = tid; j0 < nvec; j0 += NT * 8) {  // 8 loads in flight per thread
+            uint4 w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                w[u] = j0 + u * NT < nvec ? __ldg(w4 + j0 + u * NT) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cnt += __popc(w[u].x) + __popc(w[u].y) + __popc(w[u].z) + __popc(w[u].w);
         }
         cnt = __reduce_add_sync(kFull, cnt);
         if (lane == 0) s_red[warp] = cnt;
@@ -266,16 +277,16 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
 
     // One tile.  GEN: the tile holds b0 or blast (partial rows) or lies past
     // the tensor map; otherwise every row is full and comes from shared memory.
+    uint32_t st = 0, phase = 0;  // ring position of tile i: i % kStages, (i / kStages) & 1
     auto tile = [&](auto gen_tag, uint64_t i) {
         constexpr bool GEN = decltype(gen_tag)::value;
-        const int st = int(i % kStages);
         const int par = int(i & 1);
         const uint64_t t = ta + i;
         const uint64_t tile_lo = t * kTile;
         const bool smem_rows = TMA && tile_lo + kTile <= tensor_end;
         uint32_t fl;
         if (TMA) {
-            mbar_wait(&bars[st], uint32_t(i / kStages) & 1u);
+            mbar_wait(&bars[st], phase);
             fl = sbits[st * NT + tid];
         } else {
             fl = c.bitmap[t * NT + tid];
@@ -290,6 +301,12 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         }
         const Rows<true> rs{sbase + uint32_t(st) * uint32_t(sizeof(Stage)), c.A, tile_lo, c.n};
         const Rows<false> rg{0, c.A, tile_lo, c.n};
+        if (c.debug >= 1) {  // profiling: the memory pipeline alone
+            __syncthreads();
+            if (TMA && tid == 0 && i >= 1 && i - 1 + kStages < my_count) issue(i - 1 + kStages);
+            if (++st == kStages) { st = 0; phase ^= 1u; }
+            return;
+        }
         const unsigned fm = __ballot_sync(kFull, fl != 0);
         const bool dense = __popc(fm) > kDense;
 
@@ -302,17 +319,22 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
             else
                 run = row_min<false>(rg, tid, lo, jhi);
         }
+        uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (fm && !dense) {  // sparse flagged rows: one element per lane
             for (unsigned m = fm; m; m &= m - 1) {
                 const int s = __ffs(m) - 1;
                 const uint32_t ft = __shfl_sync(kFull, fl, s);
+                const int jl = __shfl_sync(kFull, jlo, s);
                 const int jh = __shfl_sync(kFull, jhi, s);
                 const uint32_t r = warp * 32 + s;
                 const int lo = 31 - __clz(ft);
                 const int32_t v = (!GEN || smem_rows) ? rs.elem(r, int(lane)) : rg.elem(r, int(lane));
-                const uint64_t key = (int(lane) >= lo && int(lane) <= jh)
-                                         ? pack_key(v, uint32_t(rs.pos(r, int(lane)))) : kNoKey;
-                const uint64_t mk = warp_min_key(key);
+                const uint64_t key = pack_key(v, uint32_t(rs.pos(r, int(lane))));
+                const uint64_t mk = warp_min_key(int(lane) >= lo && int(lane) <= jh ? key : kNoKey);
+                if ((ft & (ft - 1)) == 0) {  // one boundary: its head part now, no scan later
+                    const uint64_t mh = warp_min_key(int(lane) >= jl && int(lane) <= lo ? key : kNoKey);
+                    if (lane == uint32_t(s)) hd = mh;
+                }
                 if (lane == uint32_t(s)) run = mk;
             }
         }
@@ -397,8 +419,6 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
                 for (unsigned m = fm; m; m &= m - 1) {
                     const int s = __ffs(m) - 1;
                     const uint32_t ft = __shfl_sync(kFull, fl, s);
-                    const int jl = __shfl_sync(kFull, jlo, s);
-                    const int jh = __shfl_sync(kFull, jhi, s);
                     // open segment entering row s: rows after the previous flagged row
                     const unsigned below = fm & ((1u << s) - 1u);
                     const int pf = below ? 31 - __clz(below) : -1;
@@ -406,6 +426,20 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
                     const SegMin in = pf >= 0 ? SegMin{seg, 1} : seg_combine(cw, SegMin{seg, 0});
                     const uint64_t rank = rank_run + cp + __reduce_add_sync(kFull, int(lane) < s ? cnt : 0u);
                     if (lane == uint32_t(s)) my_rank = rank;
+                    if ((ft & (ft - 1)) == 0) {  // one boundary: area = carry + head part
+                        if (lane == uint32_t(s)) {
+                            const uint64_t val = kmin(in.k, hd);
+                            if (!in.f) {
+                                s_head = val;
+                                s_first_rank = rank;
+                            } else if (rank > 0) {
+                                c.aq[rank - 1] = val;
+                            }
+                        }
+                        continue;
+                    }
+                    const int jl = __shfl_sync(kFull, jlo, s);
+                    const int jh = __shfl_sync(kFull, jhi, s);
                     const uint32_t r = warp * 32 + s;
                     const int32_t v = (!GEN || smem_rows) ? rs.elem(r, int(lane)) : rg.elem(r, int(lane));
                     const bool inr = int(lane) >= jl && int(lane) <= jh;
@@ -443,6 +477,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         }
         carry = seg_combine(carry, xt);
         rank_run += ct;
+        if (++st == kStages) { st = 0; phase ^= 1u; }
     };
 
     for (uint64_t i = 0; i < my_count; ++i) {
@@ -490,6 +525,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
 struct ContractLaunch {
     int grid_tma = 0, grid_ldg = 0;
     size_t smem_tma = 0;
+    uint32_t stages = 0, debug = 0;
 };
 
 ContractLaunch& contract_cfg() {
@@ -498,7 +534,13 @@ ContractLaunch& contract_cfg() {
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cfg.smem_tma = 1024 + kStages * sizeof(Stage) + kStages * NT * 4 + kStages * 8;
+        const char* e = getenv("BRMQ_CONTRACT_STAGES");  // tuning knob, default 3
+        cfg.stages = e ? uint32_t(atoi(e)) : 3u;
+        const char* d = getenv("BRMQ_CONTRACT_DEBUG");
+        cfg.debug = d ? uint32_t(atoi(d)) : 0u;
+        if (cfg.stages < 2) cfg.stages = 2;
+        if (cfg.stages > kMaxStages) cfg.stages = kMaxStages;
+        cfg.smem_tma = 1024 + cfg.stages * (sizeof(Stage) + NT * 4 + 8);
         cudaFuncSetAttribute(k_contract<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(cfg.smem_tma));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<true>, NT, cfg.smem_tma);
@@ -536,7 +578,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     if (uint64_t(grid) > tiles) grid = int(tiles);
     const int gmax = int(contract_status_words() / 3);
     ContractArgs args{A, n, tma ? rows : 0, bitmap, span, aq, nb_out, aq_len, word_info,
-                      status, status + gmax, status + 2 * gmax, epoch};
+                      status, status + gmax, status + 2 * gmax, epoch, cfg.stages, cfg.debug};
     void* params[] = {&tmap, &args};
     cudaLaunchCooperativeKernel(tma ? reinterpret_cast<const void*>(k_contract<true>)
                                     : reinterpret_cast<const void*>(k_contract<false>),
