@@ -534,8 +534,8 @@ ContractLaunch& contract_cfg() {
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char* e = getenv("BRMQ_CONTRACT_STAGES");  // tuning knob, default 3
-        cfg.stages = e ? uint32_t(atoi(e)) : 3u;
+        const char* e = getenv("BRMQ_CONTRACT_STAGES");  // tuning knob, default 2
+        cfg.stages = e ? uint32_t(atoi(e)) : 2u;
         const char* d = getenv("BRMQ_CONTRACT_DEBUG");
         cfg.debug = d ? uint32_t(atoi(d)) : 0u;
         if (cfg.stages < 2) cfg.stages = 2;

@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
     __shared__ uint32_t s_tile;
     __shared__ uint32_t whist[kWarps][kRadix];
     __shared__ uint32_t thist[kRadix];
+    __shared__ uint32_t texcl[kRadix];
     __shared__ unsigned long long s_base[kRadix];
     __shared__ uint32_t s_scan[kWarps + 1];
+    __shared__ uint32_t skey[kTile], sval[kTile];  // the tile, locally sorted by digit
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const uint32_t d = threadIdx.x;  // the digit this thread publishes / looks back for
 
@@ -115,33 +117,52 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
         whist[w][d] = sum;
         sum += c;
     }
-    uint32_t gtot;
+    uint32_t gtot, ttot;
     const uint32_t gex = block_excl_sum<kThreads>(uint32_t(ghist[d]), s_scan, gtot);
+    texcl[d] = block_excl_sum<kThreads>(tcount, s_scan, ttot);
+    // look-back for digit d, 8 predecessors per round (independent loads in flight)
     uint64_t excl = 0;
     if (tile > 0) {
-        uint64_t p = tile;
-        while (p > 0) {
-            --p;
-            uint64_t sw;
-            while (true) {
-                sw = ld_relaxed_u64(status + p * kRadix + d);
-                if (status_state(sw, epoch) != kStInvalid) break;
+        int64_t p = int64_t(tile) - 1;
+        bool done = false;
+        while (!done) {
+            uint64_t w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                w[u] = p - u >= 0 ? ld_relaxed_u64(status + uint64_t(p - u) * kRadix + d) : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (done) break;
+                if (p - u < 0) { done = true; break; }
+                while (status_state(w[u], epoch) == kStInvalid)
+                    w[u] = ld_relaxed_u64(status + uint64_t(p - u) * kRadix + d);
+                excl += status_value(w[u]);
+                if (status_state(w[u], epoch) == kStInclusive) done = true;
             }
-            excl += status_value(sw);
-            if (status_state(sw, epoch) == kStInclusive) break;
+            p -= 8;
         }
         st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, excl + tcount));
     }
     s_base[d] = (unsigned long long)gex + excl;
     __syncthreads();
 
+    // 4) stage the tile in shared memory sorted by digit (stable), then write
+    //    out so that consecutive threads hit consecutive addresses of a bucket
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         if (dig[i] < 0x100u) {
-            const uint64_t out = s_base[dig[i]] + whist[warp][dig[i]] + rank[i];
-            kout[out] = key[i];
-            vout[out] = val[i];
+            const uint32_t lp = texcl[dig[i]] + whist[warp][dig[i]] + rank[i];
+            skey[lp] = key[i];
+            sval[lp] = val[i];
         }
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < ttot; s += kThreads) {
+        const uint32_t k = skey[s];
+        const uint32_t dd = (k >> shift) & 0xFFu;
+        const uint64_t out = s_base[dd] + (s - texcl[dd]);
+        kout[out] = k;
+        vout[out] = sval[s];
     }
 }
 
