@@ -202,8 +202,10 @@ def cpu_baseline(A, Q, name) -> dict:
                       "reference sources compiled unmodified (oracle/_ref)"}, out
 
 
-def time_solves(eng, torch, stream, fn, steps, warmup, flush):
-    """Per-step CUDA-event windows on the library stream; L2 flushed between steps."""
+def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2):
+    """Per-step CUDA-event windows on the library stream; L2 flushed between steps.
+    timing: library stage events (0 off, 1 every stage, 2 only the roofline kernel)."""
+    eng.set_timing(timing)
     for _ in range(warmup):
         flush.fill_(1)
         fn()
@@ -251,7 +253,6 @@ def run_ours(args) -> dict:
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
-    eng.set_timing(True)
     dA = torch.from_numpy(A).to(dev)
     dQ = torch.from_numpy(Q.view(np.int64)).to(dev)
     dAns = torch.empty(q, dtype=torch.int64, device=dev)
@@ -277,8 +278,18 @@ def run_ours(args) -> dict:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
-        ms, stages, launches = time_solves(eng, torch, stream, solve, args.steps, args.warmup, flush)
+        ms, stages, launches = time_solves(eng, torch, stream, solve, args.steps, args.warmup, flush,
+                                           timing=2)
     torch.cuda.synchronize()
+    # per-stage breakdown (every stage bracketed by events; informative, not the headline)
+    _, breakdown, _ = time_solves(eng, torch, stream, solve, 5, 1, flush, timing=1)
+    # the other endpoint-sort pipeline on the same workload (same answers)
+    variants = {variant: aggregate_value(q, 1, statistics.mean(ms))}
+    if variant != "bbst":
+        alt = "con_bitmap" if variant == "con_radix" else "con_radix"
+        ms_alt, _, _ = time_solves(eng, torch, stream, lambda: solve(v=alt), args.steps, 2, flush,
+                                   timing=0)
+        variants[alt] = aggregate_value(q, 1, statistics.mean(ms_alt))
     t_step = max_over_ranks(statistics.mean(ms), dist, dev)
     if dist:
         dist.barrier()
@@ -302,7 +313,8 @@ def run_ours(args) -> dict:
         else:
             eng.solve_batch_bbst_con(hA, hQ, 512, VARIANT_SORT[variant], out=hO)
 
-    e2e_ms, _, _ = time_solves(eng, torch, stream, solve_host, max(3, args.steps // 2), 2, flush)
+    e2e_ms, _, _ = time_solves(eng, torch, stream, solve_host, max(3, args.steps // 2), 2, flush,
+                               timing=0)
     e2e_t = statistics.mean(e2e_ms)
     if want is not None:
         assert np.array_equal(hO, want), "e2e answers differ from the reference oracle"
@@ -311,7 +323,7 @@ def run_ours(args) -> dict:
 
     # roofline of the dominant kernel
     pk = peaks()
-    dom = max(stages.items(), key=lambda kv: kv[1][0])[0]
+    dom = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
     if variant == "bbst":
         alg_bytes = 4 * n  # block_argmin reads A once
         dom_for_roof = "block_argmin"
@@ -326,7 +338,7 @@ def run_ours(args) -> dict:
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(f"{name}/{variant}/{dom_for_roof}")
-    pre_ms = sum(v[0] for k, v in stages.items() if k not in ("query", "h2d", "d2h"))
+    pre_ms = sum(v[0] for k, v in breakdown.items() if k not in ("query", "h2d", "d2h"))
     pre_bytes = 4 * n if variant == "bbst" else 4 * (info["span_hi"] - info["span_lo"] + 1) + 16 * q + 8 * max(info["boundary"] - 1, 0)
 
     rec = {
@@ -345,8 +357,9 @@ def run_ours(args) -> dict:
                      "avg_launch_ms": kt},
         "preprocess": {"ms": pre_ms, "alg_bytes": pre_bytes,
                        "gbs": pre_bytes / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None},
-        "stages_ms": {k: round(v[0], 5) for k, v in stages.items()},
+        "stages_ms": {k: round(v[0], 5) for k, v in breakdown.items()},
         "dominant_stage": dom,
+        "variants_queries_per_s": variants,
         "clocks": clk.summary(),
         "info": info,
     }
@@ -378,7 +391,8 @@ def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
                     eng.solve_batch_bbst(dA, dQ, 512, out=dO)
                 else:
                     eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[v], out=dO)
-            ms, stages, _ = time_solves(eng, torch, stream, f, 5, 2, flush)
+            ms, _, _ = time_solves(eng, torch, stream, f, 5, 2, flush, timing=0)
+            _, stages, _ = time_solves(eng, torch, stream, f, 2, 0, flush, timing=1)
             t = statistics.mean(ms)
             out.append({"q": q, "variant": v, "queries_per_s": q / (t * 1e-3), "ms": t,
                         "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}})

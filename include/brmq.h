@@ -17,7 +17,7 @@
  *     input order (types.hpp:25-29).
  *   - Errors are status codes that map 1:1 onto the reference's exception
  *     classes (BRMQ_EDOMAIN = std::domain_error, ...); brmq_last_error()
- *     returns the thread-local message.  include/batchrmq_cuda.hpp rethrows
+ *     returns the thread-local message.  include/batchrmq_b200.hpp rethrows
  *     them as the same std:: types.
  *   - A context owns one CUDA stream and a grow-only device workspace.  One
  *     context must not be used by two threads at once; distinct contexts may
@@ -72,7 +72,8 @@ enum brmq_flags {
 
 enum brmq_sort_kind { /* == batchrmq::SortKind (contraction.hpp:23) */
     BRMQ_SORT_RADIX = 0,
-    BRMQ_SORT_COMPARISON = 1
+    BRMQ_SORT_COMPARISON = 1,
+    BRMQ_SORT_BITMAP = 2 /* device presence-bitmap (1-bit counting) sort; no reference counterpart */
 };
 
 /* ------------------------------------------------------------ context */
@@ -140,8 +141,10 @@ int brmq_floor_log2(uint64_t x, uint32_t* out);
 /* --------------------------------------------------------- instrumentation */
 
 /* Per-stage device times of the last solve on this context, measured with
- * CUDA events on the context stream (only while timing is enabled; events
- * are recorded around every kernel launch and add no synchronisation). */
+ * CUDA events on the context stream (no synchronisation is added).
+ * brmq_ctx_set_timing: 0 off, 1 every stage, 2 only the HBM-bound kernel
+ * the roofline is quoted on (the contraction scan, or the block-argmin scan
+ * of BbST) -- two event nodes instead of two per stage inside a CUDA graph. */
 #define BRMQ_MAX_STAGES 16
 typedef struct brmq_stage_times {
     int count;
@@ -163,6 +166,7 @@ typedef struct brmq_solve_info {
     uint64_t span_lo;       /* contraction: boundary[0]                   */
     uint64_t span_hi;       /* contraction: boundary[last]                */
     uint32_t kernel_launches;
+    uint32_t graph;         /* 1: the solve ran as a replayed CUDA graph     */
 } brmq_solve_info;
 
 int brmq_last_solve_info(brmq_ctx* ctx, brmq_solve_info* out);

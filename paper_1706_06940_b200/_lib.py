@@ -31,7 +31,7 @@ class SolveInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("q", C.c_uint64), ("k", C.c_uint64),
                 ("blocks", C.c_uint64), ("levels", C.c_uint32),
                 ("boundary", C.c_uint64), ("span_lo", C.c_uint64), ("span_hi", C.c_uint64),
-                ("kernel_launches", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("graph", C.c_uint32)]
 
 
 # name -> (restype, argtypes): exactly the declarations of include/brmq*.h

@@ -147,8 +147,9 @@ class Engine:
     def handle(self) -> C.c_void_p:
         return self._h
 
-    def set_timing(self, on: bool = True) -> None:
-        _check(self._L.brmq_ctx_set_timing(self._h, int(on)))
+    def set_timing(self, level: int = 1) -> None:
+        """0 off, 1 every stage, 2 only the roofline kernel (see brmq.h)."""
+        _check(self._L.brmq_ctx_set_timing(self._h, int(level)))
 
     def set_stream(self, stream_ptr: int | None) -> None:
         _check(self._L.brmq_ctx_set_stream(self._h, stream_ptr or None))

@@ -6,6 +6,7 @@
 // the device path cannot run the call fails with BRMQ_ECUDA -- there is no CPU
 // fallback anywhere in this library.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -52,6 +53,22 @@ struct Control {
 
 }  // namespace
 
+struct GraphKey {
+    int kind;
+    const void* A;
+    uint64_t n;
+    const void* Q;
+    uint64_t q;
+    uint32_t k;
+    int sort_kind;
+    void* ans;
+    cudaStream_t stream;
+    bool operator==(const GraphKey& o) const {
+        return kind == o.kind && A == o.A && n == o.n && Q == o.Q && q == o.q && k == o.k &&
+               sort_kind == o.sort_kind && ans == o.ans && stream == o.stream;
+    }
+};
+
 struct brmq_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
@@ -63,14 +80,29 @@ struct brmq_ctx {
     uint32_t* bitmap = nullptr;  // persistent, kept all-zero by the contraction kernel
     size_t bitmap_words = 0;
     Control* ctl_host = nullptr;  // pinned mirror of the control block
-    uint32_t epoch = 1;
-    // timing
-    bool timing = false;
+    uint32_t* epoch_dev = nullptr;  // device epoch counter, bumped by every solve (graph-safe)
+    uint32_t epoch_host = 1;        // host mirror of *epoch_dev
+    bool use_graphs = true;
+    struct GraphEntry;
+    std::vector<GraphEntry*> graphs;
+    // timing: 0 off, 1 every stage, 2 only the roofline kernel (contract / block_argmin)
+    int timing = 0;
     std::vector<cudaEvent_t> ev;
     std::vector<std::string> stage_names;
     std::vector<uint32_t> stage_launches;
     brmq_stage_times last_times{};
     brmq_solve_info info{};
+};
+
+// A captured solve: replaying it re-runs every kernel with the same buffers;
+// the look-back epochs come from the device counter the graph itself bumps.
+struct brmq_ctx::GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+    int timing = 0;
+    std::vector<std::string> names;
+    std::vector<uint32_t> nl;
 };
 
 namespace {
@@ -87,8 +119,17 @@ struct Carve {
     }
 };
 
+void drop_graphs(brmq_ctx* c) {
+    for (auto* g : c->graphs) {
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        delete g;
+    }
+    c->graphs.clear();
+}
+
 int ensure_ws(brmq_ctx* c, size_t bytes) {
     if (bytes <= c->ws_cap) return BRMQ_OK;
+    drop_graphs(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->ws) cudaFree(c->ws);
     c->ws = nullptr;
@@ -102,6 +143,7 @@ int ensure_ws(brmq_ctx* c, size_t bytes) {
 
 int ensure_status(brmq_ctx* c, size_t bytes) {
     if (bytes <= c->st_cap) return BRMQ_OK;
+    drop_graphs(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->st) cudaFree(c->st);
     c->st = nullptr;
@@ -116,6 +158,7 @@ int ensure_status(brmq_ctx* c, size_t bytes) {
 int ensure_bitmap(brmq_ctx* c, uint64_t n) {
     const size_t words = brmq::contract_bitmap_words(n);  // whole tiles
     if (words <= c->bitmap_words) return BRMQ_OK;
+    drop_graphs(c);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->bitmap) cudaFree(c->bitmap);
     c->bitmap = nullptr;
@@ -126,16 +169,21 @@ int ensure_bitmap(brmq_ctx* c, uint64_t n) {
     return BRMQ_OK;
 }
 
-// Reserve `count` consecutive 24-bit epochs for single-pass scans.
-uint32_t take_epochs(brmq_ctx* c, uint32_t count) {
-    if (c->epoch + count >= (1u << 24)) {
-        // wrap: every status word is reset to "invalid"
-        if (c->st) cudaMemsetAsync(c->st, 0, c->st_cap, c->stream);
-        c->epoch = 1;
+__global__ void k_bump_epoch(uint32_t* epoch, uint32_t by) { *epoch += by; }
+
+// Every solve reserves `count` consecutive 24-bit epochs for its single-pass
+// scans: one tiny kernel bumps the device counter first, and each look-back
+// kernel reads *epoch_dev + its offset.  Inside a CUDA graph the bump is a node,
+// so replays get fresh epochs too.  Before the 24-bit tag would wrap, the status
+// arena is cleared and the counter restarted (outside any graph).
+int begin_epochs(brmq_ctx* c, uint32_t count) {
+    if (c->epoch_host + count + 1 >= (1u << 24)) {
+        if (c->st) CUDA_TRY(cudaMemsetAsync(c->st, 0, c->st_cap, c->stream));
+        c->epoch_host = 1;
+        CUDA_TRY(cudaMemcpyAsync(c->epoch_dev, &c->epoch_host, 4, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
     }
-    const uint32_t e = c->epoch;
-    c->epoch += count;
-    return e;
+    return BRMQ_OK;
 }
 
 // ------------------------------------------------------------------ timing
@@ -146,18 +194,41 @@ struct Timer {
         c->stage_names.clear();
         c->stage_launches.clear();
     }
+    bool active = false;
     void stage(const char* name, int launches_before) {
         (void)launches_before;
-        if (!c->timing || n >= BRMQ_MAX_STAGES) return;
-        cudaEventRecord(c->ev[2 * n], c->stream);
+        active = c->timing == 1 || (c->timing == 2 && (std::strcmp(name, "contract") == 0 ||
+                                                        std::strcmp(name, "block_argmin") == 0));
+        if (!active || n >= BRMQ_MAX_STAGES) return;
+        record(c->ev[2 * n]);
         c->stage_names.emplace_back(name);
         c->stage_launches.push_back(0);
     }
     void end(int launches) {
-        if (!c->timing || n >= BRMQ_MAX_STAGES) return;
-        cudaEventRecord(c->ev[2 * n + 1], c->stream);
+        if (!active || n >= BRMQ_MAX_STAGES) return;
+        active = false;
+        record(c->ev[2 * n + 1]);
         c->stage_launches.back() = uint32_t(launches);
         ++n;
+    }
+    // inside a stream capture the record must be an external event node
+    void record(cudaEvent_t e) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(c->stream, &st);
+        if (st == cudaStreamCaptureStatusActive)
+            cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+        else
+            cudaEventRecord(e, c->stream);
+    }
+    void reset() {
+        n = 0;
+        c->stage_names.clear();
+        c->stage_launches.clear();
+    }
+    void restore(const std::vector<std::string>& names, const std::vector<uint32_t>& nl) {
+        c->stage_names = names;
+        c->stage_launches = nl;
+        n = int(names.size());
     }
     void finish() {
         brmq_stage_times& t = c->last_times;
@@ -200,6 +271,62 @@ int bits_for(uint64_t n) {  // bit_width(n - 1): positions are < n
     return 64 - __builtin_clzll(n - 1);
 }
 
+
+// Issues one solve: `enqueue` puts every async operation of the call on the
+// context stream (ending with the D2H of the control block).  Device-pointer
+// solves are captured once per (shape, pointers, stream) into a CUDA graph and
+// replayed: one launch instead of ~10, no CPU launch gaps between kernels.
+template <class F>
+int run_solve(brmq_ctx* c, const GraphKey& key, bool graphable, Timer& tm, int& launches,
+              F&& enqueue) {
+    cudaStream_t s = c->stream;
+    if (!(graphable && c->use_graphs)) return enqueue();
+    brmq_ctx::GraphEntry* g = nullptr;
+    for (auto* e : c->graphs)
+        if (e->key == key && e->timing == c->timing) g = e;
+    if (!g) {
+        if (c->graphs.size() >= 16) {  // small LRU-less cache: drop the oldest
+            cudaGraphExecDestroy(c->graphs.front()->exec);
+            delete c->graphs.front();
+            c->graphs.erase(c->graphs.begin());
+        }
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue();
+        const cudaError_t ee = cudaStreamEndCapture(s, &graph);
+        cudaGraphExec_t exec = nullptr;
+        if (rc == BRMQ_OK && ee == cudaSuccess &&
+            cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+            cudaGraphDestroy(graph);
+            g = new brmq_ctx::GraphEntry();
+            g->key = key;
+            g->exec = exec;
+            g->launches = launches;
+            g->timing = c->timing;
+            g->names = c->stage_names;
+            g->nl = c->stage_launches;
+            c->graphs.push_back(g);
+        } else {  // not capturable here: run directly from now on
+            if (graph) cudaGraphDestroy(graph);
+            const cudaError_t why = cudaGetLastError();
+            if (getenv("BRMQ_DEBUG"))
+                fprintf(stderr, "brmq: graph capture failed (rc=%d end=%s last=%s); direct launches\n", rc,
+                        cudaGetErrorString(ee), cudaGetErrorString(why));
+            c->use_graphs = false;
+            if (rc != BRMQ_OK) return rc;
+            launches = 0;
+            tm.reset();
+            return enqueue();
+        }
+    } else {
+        launches = g->launches;
+        tm.restore(g->names, g->nl);
+    }
+    CUDA_TRY(cudaGraphLaunch(g->exec, s));
+    c->info.graph = 1;
+    return BRMQ_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -235,6 +362,12 @@ int brmq_ctx_create(brmq_ctx** out, int device) {
     }
     c->ev.resize(2 * BRMQ_MAX_STAGES);
     for (auto& x : c->ev) cudaEventCreate(&x);
+    if (cudaMalloc(&c->epoch_dev, 256) != cudaSuccess ||
+        cudaMemcpy(c->epoch_dev, &c->epoch_host, 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        brmq_ctx_destroy(c);
+        return fail(BRMQ_ECUDA, "epoch counter allocation failed");
+    }
+    if (const char* g = getenv("BRMQ_GRAPHS")) c->use_graphs = atoi(g) != 0;
     *out = c;
     return BRMQ_OK;
 }
@@ -243,7 +376,9 @@ void brmq_ctx_destroy(brmq_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    drop_graphs(c);
     for (auto& x : c->ev) cudaEventDestroy(x);
+    if (c->epoch_dev) cudaFree(c->epoch_dev);
     if (c->ws) cudaFree(c->ws);
     if (c->st) cudaFree(c->st);
     if (c->bitmap) cudaFree(c->bitmap);
@@ -262,7 +397,7 @@ void* brmq_ctx_stream(brmq_ctx* c) { return c ? static_cast<void*>(c->stream) : 
 
 int brmq_ctx_set_timing(brmq_ctx* c, int enable) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
-    c->timing = enable != 0;
+    c->timing = enable < 0 ? 0 : (enable > 2 ? 1 : enable);
     return BRMQ_OK;
 }
 
@@ -342,33 +477,39 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
     cudaStream_t s = c->stream;
     int launches = 0;
-
-    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
-    if (!dev) {
-        tm.stage("h2d", launches);
-        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
-        tm.end(0);
-    }
-    tm.stage("block_argmin", launches);
-    int l = brmq::launch_block_argmin_i32(dA, n, k, ST, s);
-    launches += l;
-    tm.end(l);
-    tm.stage("sparse_table", launches);
-    l = brmq::launch_sparse_table(ST, b, nullptr, s);
-    launches += l;
-    tm.end(l);
-    tm.stage("query", launches);
-    l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s);
-    launches += l;
-    tm.end(l);
-    if (int rc = check_status(c)) return rc;
-    if (!dev) {
-        tm.stage("d2h", launches);
-        CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
-        tm.end(0);
-    }
-    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    auto enqueue = [&]() -> int {
+        int l = 0;
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        tm.stage("block_argmin", launches);
+        l = brmq::launch_block_argmin_i32(dA, n, k, ST, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("sparse_table", launches);
+        l = brmq::launch_sparse_table(ST, b, nullptr, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("query", launches);
+        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        return BRMQ_OK;
+    };
+    const GraphKey key{0, A, n, Q, q, k, 0, answers, s};
+    if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     c->info.blocks = b;
     c->info.levels = L;
@@ -443,74 +584,85 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
     cudaStream_t s = c->stream;
-    int launches = 0, l = 0;
-
-    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
-    if (!dev) {
-        tm.stage("h2d", launches);
-        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
-        tm.end(0);
-    }
-    const uint32_t ep_contract = take_epochs(c, 1);
-    if (use_bitmap) {
-        tm.stage("collect_mark", launches);
-        l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->span, &ctl->err, s);
+    const uint32_t n_epochs = use_bitmap ? 1u : 2u + uint32_t(brmq::radix_sort_passes(bits));
+    if (int rc = begin_epochs(c, n_epochs)) return rc;
+    int launches = 0;
+    auto enqueue = [&]() -> int {
+        int l = 0;
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, n_epochs);  // epochs of this solve
+        launches += 1;
+        // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
+        if (use_bitmap) {
+            tm.stage("collect_mark", launches);
+            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->span, &ctl->err, s);
+            launches += l;
+            tm.end(l);
+        } else {
+            auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
+            auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
+            auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
+            auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
+            tm.stage("collect", launches);
+            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s);
+            launches += l;
+            tm.end(l);
+            tm.stage("radix_sort", launches);
+            bool in_alt = false;
+            l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), S(i_rst), s, &in_alt,
+                                        c->epoch_dev, 2);
+            launches += l;
+            tm.end(l);
+            tm.stage("unique_rank", launches);
+            l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr,
+                                    c->bitmap, ctl->span, &ctl->nb, &ctl->err, S(i_ust),
+                                    &ctl->tickets[0], c->epoch_dev, 1, s);
+            launches += l;
+            tm.end(l);
+        }
+        tm.stage("contract", launches);
+        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len,
+                                  use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
+                                  c->epoch_dev, 0, s);
         launches += l;
         tm.end(l);
-    } else {
-        auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
-        auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
-        auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
-        auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
-        tm.stage("collect", launches);
-        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s);
+        if (use_bitmap) {
+            tm.stage("remap", launches);
+            l = brmq::launch_remap_bitmap(dQ, q, n, reinterpret_cast<uint2*>(P(i_wi)), cl, cr, s);
+            launches += l;
+            tm.end(l);
+        }
+        tm.stage("block_argmin", launches);
+        l = brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
         launches += l;
         tm.end(l);
-        tm.stage("radix_sort", launches);
-        bool in_alt = false;
-        const uint32_t ep = take_epochs(c, uint32_t(brmq::radix_sort_passes(bits)));
-        l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), S(i_rst), s, &in_alt, ep);
+        tm.stage("sparse_table", launches);
+        l = brmq::launch_sparse_table(ST, b_max, &ctl->b_dev, s);
         launches += l;
         tm.end(l);
-        tm.stage("unique_rank", launches);
-        const uint32_t ep_u = take_epochs(c, 1);
-        l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr, c->bitmap,
-                                ctl->span, &ctl->nb, &ctl->err, S(i_ust), &ctl->tickets[0], ep_u, s);
+        tm.stage("query", launches);
+        l = brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr, q, dAns, s);
         launches += l;
         tm.end(l);
-    }
-    tm.stage("contract", launches);
-    l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len,
-                              use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
-                              ep_contract, s);
-    launches += l;
-    tm.end(l);
-    if (use_bitmap) {
-        tm.stage("remap", launches);
-        l = brmq::launch_remap_bitmap(dQ, q, n, reinterpret_cast<uint2*>(P(i_wi)), cl, cr, s);
-        launches += l;
-        tm.end(l);
-    }
-    tm.stage("block_argmin", launches);
-    l = brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
-    launches += l;
-    tm.end(l);
-    tm.stage("sparse_table", launches);
-    l = brmq::launch_sparse_table(ST, b_max, &ctl->b_dev, s);
-    launches += l;
-    tm.end(l);
-    tm.stage("query", launches);
-    l = brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr, q, dAns, s);
-    launches += l;
-    tm.end(l);
-    if (int rc = check_status(c)) return rc;
-    if (!dev) {
-        tm.stage("d2h", launches);
-        CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
-        tm.end(0);
-    }
-    if (int rc = sync_and_read_control(c, ctl)) return rc;
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        return BRMQ_OK;
+    };
+    const GraphKey key{1, A, n, Q, q, k, sort_kind, answers, s};
+    if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->epoch_host += n_epochs;
+    CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     const Control& h = *c->ctl_host;
     c->info.boundary = h.nb;
@@ -576,9 +728,11 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
     auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
     brmq::launch_split_eps(dE, m, k0, v0, s);
     bool in_alt = false;
-    const uint32_t ep = take_epochs(c, 4);
+    if (int rc = begin_epochs(c, 4)) return rc;
+    k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, 4);
+    c->epoch_host += 4;
     brmq::launch_radix_sort(k0, v0, k1, v1, m, 32, P(i_rs), reinterpret_cast<uint64_t*>(c->st), s,
-                            &in_alt, ep);
+                            &in_alt, c->epoch_dev, 0);
     brmq::launch_join_eps(in_alt ? k1 : k0, in_alt ? v1 : v0, m, dE, s);
     if (int rc = check_status(c)) return rc;
     if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));
@@ -631,9 +785,11 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     auto* bd = reinterpret_cast<uint32_t*>(P(i_bd));
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     brmq::launch_split_eps(dE, m, k, v, s);
-    const uint32_t ep_u = take_epochs(c, 1), ep_c = take_epochs(c, 1);
+    if (int rc = begin_epochs(c, 2)) return rc;
+    k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, 2);
+    c->epoch_host += 2;
     brmq::launch_unique(k, v, m, n, bd, nullptr, nullptr, c->bitmap, ctl->span, &ctl->nb, &ctl->err,
-                        S(i_ust), &ctl->tickets[0], ep_u, s);
+                        S(i_ust), &ctl->tickets[0], c->epoch_dev, 0, s);
     if (int rc = sync_and_read_control(c, ctl)) return rc;
     if (c->ctl_host->err) {
         // unsorted or out-of-range endpoints: clear any marks and report
@@ -642,7 +798,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         return map_err(c->ctl_host->err);
     }
     brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len, nullptr,
-                          S(i_cst), ep_c, s);
+                          S(i_cst), c->epoch_dev, 1, s);
     brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);
     brmq::launch_u32_to_u64(bd, &ctl->nb, m, dbo, s);
     if (int rc = check_status(c)) return rc;

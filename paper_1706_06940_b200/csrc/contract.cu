@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kThreads) k_unique(
     uint32_t* __restrict__ boundary, uint32_t* __restrict__ cleft, uint32_t* __restrict__ cright_raw,
     uint32_t* __restrict__ bitmap, uint32_t* __restrict__ span, uint64_t* __restrict__ nb_out,
     uint32_t* __restrict__ err, uint64_t* __restrict__ status, uint32_t* __restrict__ ticket,
-    uint32_t epoch) {
+    const uint32_t* __restrict__ epoch_dev, uint32_t epoch_off) {
+    const uint32_t epoch = *epoch_dev + epoch_off;
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_scan[kThreads / 32 + 1];
     __shared__ unsigned long long s_excl;
@@ -273,10 +274,10 @@ size_t unique_status_words(uint64_t m) { return (m + kTile - 1) / kTile; }
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n, uint32_t* boundary,
                   uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* span,
                   uint64_t* nb_out, uint32_t* err, uint64_t* status, uint32_t* ticket,
-                  uint32_t epoch, cudaStream_t s) {
+                  const uint32_t* epoch_dev, uint32_t epoch_off, cudaStream_t s) {
     if (m == 0) return 0;
     k_unique<<<unsigned((m + kTile - 1) / kTile), kThreads, 0, s>>>(
-        pos, org, m, n, boundary, cleft, cright_raw, bitmap, span, nb_out, err, status, ticket, epoch);
+        pos, org, m, n, boundary, cleft, cright_raw, bitmap, span, nb_out, err, status, ticket, epoch_dev, epoch_off);
     return 1;
 }
 

@@ -178,7 +178,8 @@ struct ContractArgs {
     uint64_t* st_count;  // [G] epoch-tagged counts (phase A)
     uint64_t* st_part;   // [G] epoch-tagged partial descriptors (phase C)
     uint64_t* key_tail;  // [G]
-    uint32_t epoch;
+    const uint32_t* epoch_dev;  // device epoch counter (bumped once per solve)
+    uint32_t epoch_off;
     uint32_t stages;  // TMA ring depth, 2..kMaxStages
     uint32_t debug;   // profiling knob: 1 = stream only (no compute)
 };
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
 
     const uint32_t b0 = ~c.span[0], blast = c.span[1];
     if (b0 > blast) return;
+    const uint32_t epoch = *c.epoch_dev + c.epoch_off;
     const uint64_t tfirst = b0 / kTile, tlast = blast / kTile;
     const uint64_t G = gridDim.x, cta = blockIdx.x;
     const uint64_t R = (tlast - tfirst + G) / G;  // ceil(#tiles / G)
@@ -250,11 +252,11 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
             uint32_t tot = lane < NW ? s_red[lane] : 0;
             tot = __reduce_add_sync(kFull, tot);
             if (lane == 0)
-                st_release_u64(c.st_count + cta, status_pack(c.epoch, kStAggregate, tot != 0, tot));
+                st_release_u64(c.st_count + cta, status_pack(epoch, kStAggregate, tot != 0, tot));
             uint64_t sum = 0;
             for (uint64_t j = lane; j < cta; j += 32) {
                 uint64_t sw;
-                while (status_state(sw = ld_acquire_u64(c.st_count + j), c.epoch) == kStInvalid) {
+                while (status_state(sw = ld_acquire_u64(c.st_count + j), epoch) == kStInvalid) {
                 }
                 sum += status_value(sw);
             }
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
     if (warp == 0) {
         if (lane == 0) {
             c.key_tail[cta] = carry.k;
-            st_release_u64(c.st_part + cta, status_pack(c.epoch, kStInclusive, carry.f != 0, 0));
+            st_release_u64(c.st_part + cta, status_pack(epoch, kStInclusive, carry.f != 0, 0));
         }
         if (carry.f && ta != tfirst) {
             const uint64_t head = s_head;
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
                 uint64_t sw = 0, k = kNoKey;
                 bool has = false;
                 if (j >= 0) {
-                    while (status_state(sw = ld_acquire_u64(c.st_part + j), c.epoch) == kStInvalid) {
+                    while (status_state(sw = ld_acquire_u64(c.st_part + j), epoch) == kStInvalid) {
                     }
                     has = status_flag(sw);
                     k = ld_relaxed_u64(c.key_tail + j);
@@ -564,7 +566,8 @@ size_t contract_status_words() {
 
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
                     uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
-                    uint64_t* status, uint32_t epoch, cudaStream_t s) {
+                    uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
+                    cudaStream_t s) {
     if (n == 0) return 0;
     const ContractLaunch& cfg = contract_cfg();
     CUtensorMap tmap;
@@ -578,7 +581,8 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     if (uint64_t(grid) > tiles) grid = int(tiles);
     const int gmax = int(contract_status_words() / 3);
     ContractArgs args{A, n, tma ? rows : 0, bitmap, span, aq, nb_out, aq_len, word_info,
-                      status, status + gmax, status + 2 * gmax, epoch, cfg.stages, cfg.debug};
+                      status, status + gmax, status + 2 * gmax, epoch_dev, epoch_off, cfg.stages,
+                      cfg.debug};
     void* params[] = {&tmap, &args};
     cudaLaunchCooperativeKernel(tma ? reinterpret_cast<const void*>(k_contract<true>)
                                     : reinterpret_cast<const void*>(k_contract<false>),

@@ -39,11 +39,11 @@ size_t radix_sort_temp_bytes(uint64_t m, int bits);     // zeroed scratch (histo
 size_t radix_sort_status_words(uint64_t m, int bits);   // epoch-tagged look-back words
 int radix_sort_passes(int bits);
 // Stable LSD sort of (key, value) u32 pairs by the low `bits` key bits; uses
-// epochs epoch_base .. epoch_base + passes - 1.  *result_in_alt tells whether
+// epochs *epoch_dev + epoch_off .. + passes - 1 (device counter, see api.cu).  *result_in_alt tells whether
 // the sorted data ended in alt_keys / alt_vals.
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
                       uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
-                      bool* result_in_alt, uint32_t epoch_base);
+                      bool* result_in_alt, const uint32_t* epoch_dev, uint32_t epoch_off);
 
 // ---------------------------------------------------------------- contract.cu
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
@@ -52,7 +52,7 @@ size_t unique_status_words(uint64_t m);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
                   uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
-                  uint32_t* ticket, uint32_t epoch, cudaStream_t s);
+                  uint32_t* ticket, const uint32_t* epoch_dev, uint32_t epoch_off, cudaStream_t s);
 size_t contract_tiles(uint64_t n);  // 8192-element tiles over A
 size_t contract_bitmap_words(uint64_t n);  // bitmap words the contraction reads (whole tiles)
 size_t contract_status_words();    // status-arena words the contraction needs
@@ -61,7 +61,8 @@ size_t contract_status_words();    // status-arena words the contraction needs
 // (rank prefix, bits) of every non-empty bitmap word, which is cleared.
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
                     uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
-                    uint64_t* status, uint32_t epoch, cudaStream_t s);
+                    uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
+                    cudaStream_t s);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)

@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
                                                       const unsigned long long* __restrict__ ghist,
                                                       uint64_t* __restrict__ status,
                                                       uint32_t* __restrict__ ticket,
-                                                      uint32_t epoch) {
+                                                      const uint32_t* __restrict__ epoch_dev,
+                                                      uint32_t epoch_off) {
+    const uint32_t epoch = *epoch_dev + epoch_off;
     __shared__ uint32_t s_tile;
     __shared__ uint32_t whist[kWarps][kRadix];
     __shared__ uint32_t thist[kRadix];
@@ -180,7 +182,7 @@ int radix_sort_passes(int bits) { return bits <= 0 ? 0 : (bits + 7) / 8; }
 
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
                       uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
-                      bool* result_in_alt, uint32_t epoch_base) {
+                      bool* result_in_alt, const uint32_t* epoch_dev, uint32_t epoch_off) {
     *result_in_alt = false;
     if (m <= 1 || bits <= 0) return 0;
     const int passes = (bits + 7) / 8;
@@ -200,11 +202,10 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
     uint32_t* kout = alt_keys;
     uint32_t* vout = alt_vals;
     for (int p = 0; p < passes; ++p) {
-        const uint32_t epoch = epoch_base + uint32_t(p);
         k_rs_pass<<<unsigned(tiles), kThreads, 0, stream>>>(kin, vin, kout, vout, m, 8 * p,
                                                             ghist + p * kRadix,
                                                             status + uint64_t(p) * tiles * kRadix,
-                                                            tickets + p, epoch);
+                                                            tickets + p, epoch_dev, epoch_off + uint32_t(p));
         ++launches;
         const uint32_t* tk = kin;
         const uint32_t* tv = vin;
