@@ -47,8 +47,9 @@
 namespace brmq {
 namespace {
 
-constexpr int NT = 128;             // threads per CTA
-constexpr int NW = NT / 32;         // warps per CTA
+constexpr int NT = 128;             // consumer threads per CTA (one row each)
+constexpr int NW = NT / 32;         // consumer warps per CTA
+constexpr int NTP = NT + 32;        // + one producer warp issuing the TMA ring
 constexpr int kRow = 32;            // positions per thread = one 128-byte row
 constexpr int kTile = NT * kRow;    // 4096 positions = 16 KB per tile
 constexpr int kMaxStages = 4;       // TMA ring depth (runtime: ContractArgs::stages)
@@ -98,21 +99,20 @@ __device__ __forceinline__ int32_t comp(const int4& x, int e) {
 template <bool FULL, class RW>
 __device__ __forceinline__ uint64_t row_min(const RW& rw, uint32_t r, int lo, int hi) {
     if (FULL || (lo == 0 && hi == kRow - 1)) {
+        // min per 16-byte chunk (3-way mins), leftmost winning chunk by strict '<',
+        // then the leftmost element of that chunk equal to the minimum
         int4 x = rw.chunk(r, 0);
-        int32_t bv = x.x;
-        int bi = 0;
-        if (x.y < bv) { bv = x.y; bi = 1; }
-        if (x.z < bv) { bv = x.z; bi = 2; }
-        if (x.w < bv) { bv = x.w; bi = 3; }
+        int32_t bv = __vimin3_s32(x.x, x.y, min(x.z, x.w));
+        int bc = 0;
 #pragma unroll
         for (int c = 1; c < 8; ++c) {
             x = rw.chunk(r, c);
-            if (x.x < bv) { bv = x.x; bi = 4 * c; }
-            if (x.y < bv) { bv = x.y; bi = 4 * c + 1; }
-            if (x.z < bv) { bv = x.z; bi = 4 * c + 2; }
-            if (x.w < bv) { bv = x.w; bi = 4 * c + 3; }
+            const int32_t m = __vimin3_s32(x.x, x.y, min(x.z, x.w));
+            if (m < bv) { bv = m; bc = c; }
         }
-        return pack_key(bv, uint32_t(rw.pos(r, bi)));
+        x = rw.chunk(r, bc);
+        const int e = x.x == bv ? 0 : x.y == bv ? 1 : x.z == bv ? 2 : 3;
+        return pack_key(bv, uint32_t(rw.pos(r, 4 * bc + e)));
     }
     int32_t bv = 0x7FFFFFFF;
     int bi = -1;
@@ -185,7 +185,7 @@ struct ContractArgs {
 };
 
 template <bool TMA>
-__global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtensorMap tmap,
                                                  const ContractArgs c) {
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -194,10 +194,11 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
     Stage* stg = reinterpret_cast<Stage*>(base_ptr);
     const uint32_t kStages = c.stages;
     uint32_t* sbits = reinterpret_cast<uint32_t*>(base_ptr + (TMA ? kStages * sizeof(Stage) : 0));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sbits + (TMA ? kStages * NT : 0));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbits + (TMA ? kStages * NT : 0));  // full[S]
+    uint64_t* empties = bars + kMaxStages;                                             // empty[S]
     __shared__ uint64_t s_tk[2][NW];  // double-buffered warp totals of the tile scan
     __shared__ uint32_t s_tf[2][NW], s_tc[2][NW];
-    __shared__ uint32_t s_red[NW];
+    __shared__ uint32_t s_red[NW + 1];
     __shared__ unsigned long long s_base;
     __shared__ uint64_t s_head;  // partial of the area closed by the range's first boundary
     __shared__ unsigned long long s_first_rank;
@@ -222,12 +223,18 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         tma_load_2d(stg[st].a, &tmap, 0, int(t * NT), &bars[st]);
         bulk_g2s(sbits + st * NT, c.bitmap + t * NT, NT * 4u, &bars[st]);
     };
+    const bool producer = warp == NW;
     if (TMA && tid == 0) {
-        for (uint32_t st = 0; st < kStages; ++st) mbar_init(&bars[st], 1);
+        for (uint32_t st = 0; st < kStages; ++st) {
+            mbar_init(&bars[st], 1);       // TMA bytes land
+            mbar_init(&empties[st], NW);   // every consumer warp is done with the stage
+        }
         fence_mbar_init();
-        for (uint64_t i = 0; i < my_count && i < uint64_t(kStages); ++i) issue(i);
     }
     if (tid == 0) s_head = kNoKey;
+    __syncthreads();
+    if (TMA && producer && lane == 0)  // prologue: the first kStages tiles, before phase A
+        for (uint64_t i = 0; i < my_count && i < uint64_t(kStages); ++i) issue(i);
 
     // ---- A: boundaries in the range, published at once; base = sum of predecessors
     if (c.debug == 2) {
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         const uint4* w4 = reinterpret_cast<const uint4*>(c.bitmap + ta * NT);
         const uint64_t nvec = my_count * (NT / 4);
         uint32_t cnt = 0;
-        for (uint64_t j0 = tid; j0 < nvec; j0 += NT * 8) {  // 8 loads in flight per thread
+        for (uint64_t j0 = tid; !producer && j0 < nvec; j0 += NT * 8) {  // 8 loads in flight per thread
             uint4 w[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -249,16 +256,25 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         if (lane == 0) s_red[warp] = cnt;
         __syncthreads();
         if (warp == 0) {
-            uint32_t tot = lane < NW ? s_red[lane] : 0;
+            uint32_t tot = lane < NW + 1 ? s_red[lane] : 0;
             tot = __reduce_add_sync(kFull, tot);
             if (lane == 0)
                 st_release_u64(c.st_count + cta, status_pack(epoch, kStAggregate, tot != 0, tot));
+            // the counts live inside the status words: relaxed loads suffice, and
+            // 4 independent loads per lane stay in flight (no acquire / L1 flush)
             uint64_t sum = 0;
-            for (uint64_t j = lane; j < cta; j += 32) {
-                uint64_t sw;
-                while (status_state(sw = ld_acquire_u64(c.st_count + j), epoch) == kStInvalid) {
+            for (uint64_t j0 = lane; j0 < cta; j0 += 128) {
+                uint64_t sw[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    sw[u] = j0 + 32 * u < cta ? ld_relaxed_u64(c.st_count + j0 + 32 * u) : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (j0 + 32 * u >= cta) break;
+                    while (status_state(sw[u], epoch) == kStInvalid)
+                        sw[u] = ld_relaxed_u64(c.st_count + j0 + 32 * u);
+                    sum += status_value(sw[u]);
                 }
-                sum += status_value(sw);
             }
             sum = warp_sum_u64(sum);
             if (lane == 0) {
@@ -273,6 +289,15 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
     }
 
     // ---- B: stream the range
+    if (producer) {  // refill each stage as soon as all consumer warps released it
+        if (TMA && lane == 0)
+            for (uint64_t i = kStages; i < my_count; ++i) {
+                const uint32_t st = uint32_t(i % kStages);
+                mbar_wait(&empties[st], uint32_t(i / kStages - 1) & 1u);
+                issue(i);
+            }
+        return;
+    }
     SegMin carry{kNoKey, 0};  // open segment after the tiles done so far (block-uniform)
     uint64_t rank_run = s_base;
     const uint64_t tensor_end = c.rows * 32;  // positions >= this are read from global
@@ -304,8 +329,8 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         const Rows<true> rs{sbase + uint32_t(st) * uint32_t(sizeof(Stage)), c.A, tile_lo, c.n};
         const Rows<false> rg{0, c.A, tile_lo, c.n};
         if (c.debug >= 1) {  // profiling: the memory pipeline alone
-            __syncthreads();
-            if (TMA && tid == 0 && i >= 1 && i - 1 + kStages < my_count) issue(i - 1 + kStages);
+            __syncwarp();
+            if (TMA && lane == 0) mbar_arrive(&empties[st]);
             if (++st == kStages) { st = 0; phase ^= 1u; }
             return;
         }
@@ -375,9 +400,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
             s_tf[par][warp] = wt.f;
             s_tc[par][warp] = wc;
         }
-        __syncthreads();  // the only block barrier of the tile
-        // every thread is past the previous tile: refill its stage
-        if (TMA && tid == 0 && i >= 1 && i - 1 + kStages < my_count) issue(i - 1 + kStages);
+        bar_sync_named(1, NT);  // the only consumer barrier of the tile
         SegMin wp{kNoKey, 0}, xt{kNoKey, 0};
         uint32_t cp = 0, ct = 0;
 #pragma unroll
@@ -479,6 +502,8 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         }
         carry = seg_combine(carry, xt);
         rank_run += ct;
+        __syncwarp();
+        if (TMA && lane == 0) mbar_arrive(&empties[st]);  // this warp is done with the stage
         if (++st == kStages) { st = 0; phase ^= 1u; }
     };
 
@@ -490,7 +515,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
         if (interior) tile(std::false_type{}, i);
         else tile(std::true_type{}, i);
     }
-    __syncthreads();  // s_head / s_first_rank visible
+    bar_sync_named(1, NT);  // s_head / s_first_rank visible (consumers only)
 
     // ---- C: stitch the area that crosses into this range from the left
     if (warp == 0) {
@@ -508,11 +533,12 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ CUtenso
                 uint64_t sw = 0, k = kNoKey;
                 bool has = false;
                 if (j >= 0) {
-                    while (status_state(sw = ld_acquire_u64(c.st_part + j), epoch) == kStInvalid) {
+                    while (status_state(sw = ld_relaxed_u64(c.st_part + j), epoch) == kStInvalid) {
                     }
                     has = status_flag(sw);
-                    k = ld_relaxed_u64(c.key_tail + j);
                 }
+                __threadfence();  // acquire: the tails were stored before their descriptors
+                if (j >= 0) k = ld_relaxed_u64(c.key_tail + j);
                 const unsigned hm = __ballot_sync(kFull, has || j < 0);
                 const int g = hm ? __ffs(hm) - 1 : 32;
                 acc = kmin(acc, warp_min_key(int(lane) <= g ? k : kNoKey));
@@ -542,12 +568,12 @@ ContractLaunch& contract_cfg() {
         cfg.debug = d ? uint32_t(atoi(d)) : 0u;
         if (cfg.stages < 2) cfg.stages = 2;
         if (cfg.stages > kMaxStages) cfg.stages = kMaxStages;
-        cfg.smem_tma = 1024 + cfg.stages * (sizeof(Stage) + NT * 4 + 8);
+        cfg.smem_tma = 1024 + cfg.stages * (sizeof(Stage) + NT * 4) + 2 * kMaxStages * 8;
         cudaFuncSetAttribute(k_contract<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(cfg.smem_tma));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<true>, NT, cfg.smem_tma);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<true>, NTP, cfg.smem_tma);
         cfg.grid_tma = sms * (per > 0 ? per : 1);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<false>, NT, 1024);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<false>, NTP, 1024 + 2 * kMaxStages * 8);
         cfg.grid_ldg = sms * (per > 0 ? per : 1);
     }
     return cfg;
@@ -586,7 +612,8 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     void* params[] = {&tmap, &args};
     cudaLaunchCooperativeKernel(tma ? reinterpret_cast<const void*>(k_contract<true>)
                                     : reinterpret_cast<const void*>(k_contract<false>),
-                                dim3(grid), dim3(NT), params, tma ? cfg.smem_tma : 1024, s);
+                                dim3(grid), dim3(NTP), params,
+                                tma ? cfg.smem_tma : 1024 + 2 * kMaxStages * 8, s);
     return 1;  // launch errors surface through the caller's cudaGetLastError
 }
 

@@ -25,8 +25,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096 keys
+constexpr int kItemsLarge = 16;  // 4096-key tiles for large batches
+constexpr int kItemsSmall = 4;   // 1024-key tiles: 4x shorter per-tile latency for small ones
+constexpr uint64_t kSmallM = 1u << 18;
+inline int items_for(uint64_t m) { return m <= kSmallM ? kItemsSmall : kItemsLarge; }
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 4;
 
@@ -48,6 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_hist(const uint32_t* __restrict
     }
 }
 
+template <int kItems>
 __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict__ kin,
                                                       const uint32_t* __restrict__ vin,
                                                       uint32_t* __restrict__ kout,
@@ -59,6 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ epoch_dev,
                                                       uint32_t epoch_off) {
     const uint32_t epoch = *epoch_dev + epoch_off;
+    constexpr int kTile = kThreads * kItems;
     __shared__ uint32_t s_tile;
     __shared__ uint32_t whist[kWarps][kRadix];
     __shared__ uint32_t thist[kRadix];
@@ -175,7 +179,8 @@ size_t radix_sort_temp_bytes(uint64_t, int) { return size_t(kMaxPasses * kRadix 
 
 size_t radix_sort_status_words(uint64_t m, int bits) {
     const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
-    return size_t(passes) * ((m + kTile - 1) / kTile) * kRadix;
+    const uint64_t tile = uint64_t(kThreads) * items_for(m);
+    return size_t(passes) * ((m + tile - 1) / tile) * kRadix;
 }
 
 int radix_sort_passes(int bits) { return bits <= 0 ? 0 : (bits + 7) / 8; }
@@ -186,7 +191,8 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
     *result_in_alt = false;
     if (m <= 1 || bits <= 0) return 0;
     const int passes = (bits + 7) / 8;
-    const uint64_t tiles = (m + kTile - 1) / kTile;
+    const int items = items_for(m);
+    const uint64_t tiles = (m + uint64_t(kThreads) * items - 1) / (uint64_t(kThreads) * items);
     auto* ghist = static_cast<unsigned long long*>(tmp);
     auto* tickets = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8);
     cudaMemsetAsync(tmp, 0, radix_sort_temp_bytes(m, bits), stream);
@@ -202,7 +208,8 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
     uint32_t* kout = alt_keys;
     uint32_t* vout = alt_vals;
     for (int p = 0; p < passes; ++p) {
-        k_rs_pass<<<unsigned(tiles), kThreads, 0, stream>>>(kin, vin, kout, vout, m, 8 * p,
+        auto kern = items == kItemsSmall ? k_rs_pass<kItemsSmall> : k_rs_pass<kItemsLarge>;
+        kern<<<unsigned(tiles), kThreads, 0, stream>>>(kin, vin, kout, vout, m, 8 * p,
                                                             ghist + p * kRadix,
                                                             status + uint64_t(p) * tiles * kRadix,
                                                             tickets + p, epoch_dev, epoch_off + uint32_t(p));
