@@ -20,13 +20,23 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;  // 16-byte vectors per lane in flight
 
-// k % 128 == 0, A 16-byte aligned: full blocks [0, nfull).
+// k % 128 == 0, A 16-byte aligned: full blocks [0, nfull) with vector loads;
+// the trailing partial block (blk == nfull < nblk) with lane-strided scalars.
 __global__ void __launch_bounds__(kThreads) k_block_argmin_i32_vec(const int32_t* __restrict__ A,
-                                                                   uint64_t nfull, uint32_t k,
+                                                                   uint64_t n, uint64_t nfull,
+                                                                   uint64_t nblk, uint32_t k,
                                                                    uint64_t* __restrict__ keys) {
     const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    if (blk >= nfull) return;
+    if (blk >= nblk) return;
     const unsigned lane = lane_id();
+    if (blk >= nfull) {  // clipped trailing block
+        const uint64_t lo = blk * k;
+        uint64_t best = kNoKey;
+        for (uint64_t i = lo + lane; i < n; i += 32) best = kmin(best, pack_key(__ldg(A + i), uint32_t(i)));
+        best = warp_min_key(best);
+        if (lane == 0) keys[blk] = best;
+        return;
+    }
     const uint32_t base_pos = uint32_t(blk * k);
     const int4* v4 = reinterpret_cast<const int4*>(A + uint64_t(base_pos));
     const uint32_t nvec = k >> 2;  // multiple of 32
@@ -116,22 +126,12 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
                             cudaStream_t stream) {
     const uint64_t nblk = (n + k - 1) / k;
     if (nblk == 0) return 0;
-    int launches = 0;
-    uint64_t done = 0;
     if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
-        const uint64_t nfull = n / k;
-        if (nfull) {
-            k_block_argmin_i32_vec<<<grid_for_warps(nfull), kThreads, 0, stream>>>(A, nfull, k, keys);
-            ++launches;
-        }
-        done = nfull;
+        k_block_argmin_i32_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys);
+    } else {
+        k_block_argmin_i32_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, k, 0, nblk, keys);
     }
-    if (done < nblk) {
-        k_block_argmin_i32_gen<<<grid_for_warps(nblk - done), kThreads, 0, stream>>>(A, n, k, done,
-                                                                                     nblk, keys);
-        ++launches;
-    }
-    return launches;
+    return 1;
 }
 
 int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,

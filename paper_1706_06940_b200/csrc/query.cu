@@ -244,21 +244,23 @@ template <class QP>
 void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
                   uint64_t* ans, cudaStream_t s) {
     const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0;
-    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 4>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 8>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 2>(e, qp, k, ST, stride, q, ans, s);
+    // one pending range per round: fewer registers -> more resident warps, which
+    // beats batching ranges per round on this latency-bound kernel (measured)
+    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s);
     if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 16>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 4>(e, qp, k, ST, stride, q, ans, s);
     return launch_q<ElemI32, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
 }
 
 template <class QP>
 void dispatch_key(ElemKey e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
                   uint64_t* ans, cudaStream_t s) {
-    if (k == 512) return launch_q<ElemKey, QP, 8, 2>(e, qp, k, ST, stride, q, ans, s);
-    if (k == 256) return launch_q<ElemKey, QP, 4, 4>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 512) return launch_q<ElemKey, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 256) return launch_q<ElemKey, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s);
     if (k == 1024) return launch_q<ElemKey, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (k == 128) return launch_q<ElemKey, QP, 2, 8>(e, qp, k, ST, stride, q, ans, s);
+    if (k == 128) return launch_q<ElemKey, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s);
     return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
 }
 

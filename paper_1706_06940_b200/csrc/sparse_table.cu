@@ -11,64 +11,76 @@
 // "t" positions (column = r + s*t) plus a halo of 2^D - 1 t-positions,
 // doubles D times in shared memory (ping-pong buffers, one barrier per level)
 // and writes each finished level straight to its row.  base = 0 uses R = 1
-// (plain contiguous columns, D <= 10); higher bases use R = 8 residues so
-// every global access is a 64-byte contiguous run.  b = 2M (n = 2^30,
-// k = 512, 22 levels) needs 3 launches instead of 21.
+// (plain contiguous columns, D <= 10, T = 2048); higher bases use R = 16
+// residues (128-byte runs, D <= 7, T = 64).  The loops are split so that the
+// store predicate is a single 32-bit compare against a per-level limit.
+// b = 2M (n = 2^30, k = 512, 22 levels) needs 3 launches instead of 21.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace brmq {
 namespace {
 
-constexpr int kThreads = 256;
-
-template <int R>
-__global__ void __launch_bounds__(kThreads) k_st_tile(uint64_t* __restrict__ ST, uint64_t b_max,
-                                                      const uint64_t* __restrict__ b_dev,
-                                                      uint32_t base, uint32_t D, uint32_t T,
-                                                      uint64_t groups) {
+template <int R, int T, int NT>
+__global__ void __launch_bounds__(NT) k_st_tile(uint64_t* __restrict__ ST, uint64_t b_max,
+                                                const uint64_t* __restrict__ b_dev, uint32_t base,
+                                                uint32_t D, uint32_t groups) {
     extern __shared__ uint64_t smem[];
     const uint64_t b = b_dev ? *b_dev : b_max;
     const uint64_t s = 1ull << base;
-    const uint32_t H = (1u << D) - 1;
-    const uint32_t W = T + H;
-    const uint64_t g = blockIdx.x % groups;         // residue group
-    const uint64_t tt = blockIdx.x / groups;        // t tile
-    const uint64_t r0 = g * R;
-    const uint64_t t0 = tt * T;
-    if (b < s || r0 + s * t0 + s > b) return;       // no valid level-`base` cell in this tile
-    uint64_t* buf0 = smem;
-    uint64_t* buf1 = smem + size_t(W) * R;
+    const uint32_t W = T + (1u << D) - 1;
+    const uint32_t g = blockIdx.x % groups;  // residue group
+    const uint32_t tt = blockIdx.x / groups;  // t tile
+    const uint64_t r0 = uint64_t(g) * R;
+    const uint64_t t0 = uint64_t(tt) * T;
+    if (b < s || r0 + s * t0 + s > b) return;  // no valid level-`base` cell in this tile
+    uint64_t* cur = smem;
+    uint64_t* nxt = smem + size_t(W) * R;
     const uint64_t* row_in = ST + uint64_t(base) * b_max;
-    const uint64_t last_valid = b - s;              // level-base cell c valid iff c <= b - 2^base
-    for (uint32_t idx = threadIdx.x; idx < W * R; idx += kThreads) {
-        const uint32_t rl = idx % R, tl = idx / R;
-        const uint64_t c = r0 + rl + s * (t0 + tl);
-        buf0[idx] = c <= last_valid ? row_in[c] : kNoKey;
+    // level-`base` cell (r, t) is valid iff r + s*t <= b - s  <=>  t <= (b - s - r) >> base
+    for (uint32_t i = threadIdx.x; i < W * R; i += NT) {
+        const uint32_t rl = i % R, tl = i / R;
+        const uint64_t c = r0 + rl + ((t0 + tl) << base);
+        cur[i] = c + s <= b ? row_in[c] : kNoKey;
     }
     __syncthreads();
-    uint64_t* cur = buf0;
-    uint64_t* nxt = buf1;
     for (uint32_t d = 1; d <= D; ++d) {
         const uint32_t half = 1u << (d - 1);
-        const uint32_t live = W - half;             // t positions with both operands in window
+        const uint32_t live = (W - half) * R;  // items with both operands in the window
         const uint32_t lvl = base + d;
         const uint64_t span = 1ull << lvl;
-        uint64_t* row_out = ST + uint64_t(lvl) * b_max;
-        for (uint32_t idx = threadIdx.x; idx < live * R; idx += kThreads) {
-            const uint64_t v = kmin(cur[idx], cur[idx + half * R]);
-            nxt[idx] = v;
-            const uint32_t rl = idx % R, tl = idx / R;
-            if (tl < T) {
-                const uint64_t c = r0 + rl + s * (t0 + tl);
-                if (c + span <= b) row_out[c] = v;
-            }
+        uint64_t* row_out = ST + uint64_t(lvl) * b_max + r0 + (t0 << base);
+        // stored cells: tl < T and column + span <= b
+        const int64_t room = int64_t(b) - int64_t(span) - int64_t(r0) - int64_t(t0 << base);
+        const uint32_t stored = T * R;
+        for (uint32_t i = threadIdx.x; i < stored; i += NT) {
+            const uint64_t v = kmin(cur[i], cur[i + half * R]);
+            nxt[i] = v;
+            const uint32_t rl = i % R, tl = i / R;
+            const int64_t off = int64_t(rl) + (int64_t(tl) << base);
+            if (off <= room) row_out[off] = v;
         }
+        for (uint32_t i = stored + threadIdx.x; i < live; i += NT)
+            nxt[i] = kmin(cur[i], cur[i + half * R]);
         __syncthreads();
         uint64_t* t = cur;
         cur = nxt;
         nxt = t;
     }
+}
+
+template <int R, int T, int NT>
+int launch_tile(uint64_t* ST, uint64_t b, const uint64_t* b_dev, uint32_t base, uint32_t D,
+                cudaStream_t stream) {
+    const uint64_t s = 1ull << base;
+    const uint64_t groups = s >= uint64_t(R) ? s / R : 1;
+    const uint64_t tcount = (b + s - 1) / s;
+    const uint64_t tiles = (tcount + T - 1) / T;
+    const size_t sm = size_t(2) * (T + (1u << D) - 1) * R * sizeof(uint64_t);
+    cudaFuncSetAttribute(k_st_tile<R, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    k_st_tile<R, T, NT><<<unsigned(groups * tiles), NT, sm, stream>>>(ST, b, b_dev, base, D,
+                                                                      uint32_t(groups));
+    return 1;
 }
 
 }  // namespace
@@ -81,26 +93,15 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
     while (base < L - 1) {
         if (base == 0) {
             const uint32_t D = (L - 1) < 10 ? (L - 1) : 10;
-            const uint32_t T = b >= 65536 ? 256 : 1024;  // >= 2-5 CTAs per SM on big tables
-            const uint64_t tiles = (b + T - 1) / T;
-            const size_t sm = size_t(2) * (T + (1u << D) - 1) * sizeof(uint64_t);
-            cudaFuncSetAttribute(k_st_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_st_tile<1><<<unsigned(tiles), kThreads, sm, stream>>>(ST, b, b_dev, 0, D, T, 1);
+            // small tables: narrow tiles so that several CTAs share the work
+            launches += b >= (1u << 16) ? launch_tile<1, 2048, 512>(ST, b, b_dev, 0, D, stream)
+                                        : launch_tile<1, 256, 256>(ST, b, b_dev, 0, D, stream);
             base = D;
         } else {
             const uint32_t D = (L - 1 - base) < 7 ? (L - 1 - base) : 7;
-            const uint32_t T = 32;
-            const uint64_t s = 1ull << base;
-            const uint64_t groups = s / 8;  // base >= 10 here; 8 residues = 64-byte runs
-            const uint64_t tcount = (b + s - 1) / s;
-            const uint64_t tiles = (tcount + T - 1) / T;
-            const size_t sm = size_t(2) * (T + (1u << D) - 1) * 8 * sizeof(uint64_t);
-            cudaFuncSetAttribute(k_st_tile<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_st_tile<8><<<unsigned(groups * tiles), kThreads, sm, stream>>>(ST, b, b_dev, base, D, T,
-                                                                             groups);
+            launches += launch_tile<16, 64, 256>(ST, b, b_dev, base, D, stream);  // base >= 10
             base += D;
         }
-        ++launches;
     }
     return launches;
 }

@@ -1,0 +1,15 @@
+import sys, statistics, json, numpy as np, torch
+sys.path.insert(0, '.')
+from bench import gen_workload, time_solves
+from paper_1706_06940_b200 import Engine
+res = {}
+for cfg in ('c3', 'c4', 'c5'):
+    A, Q = gen_workload(cfg)
+    eng = Engine(0)
+    s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
+    dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+    ms, st, _ = time_solves(eng, torch, s, lambda: eng.solve_batch_bbst(dA, dQ, 512), 3, 1, flush, timing=1)
+    res[cfg] = {k: round(v[0], 4) for k, v in st.items()}
+    del dA, dQ, A, Q; eng.close(); torch.cuda.empty_cache()
+print(json.dumps(res))
