@@ -196,4 +196,18 @@ inline Answers solve_batch_bbst(std::span<const Value> array, const QueryBatch& 
     return out;
 }
 
+// SPEC.md:266-310 with a LevelConfig chain (h = 1, or h = 2 with k_1 = 32)
+struct LevelConfig {
+    std::vector<std::uint32_t> block_sizes{512};
+};
+inline Answers solve_batch_bbst(std::span<const Value> array, const QueryBatch& batch,
+                                const LevelConfig& cfg) {
+    Answers out(batch.size());
+    b200::check(brmq_solve_bbst_ml(b200::context().get(), array.data(), array.size(),
+                                   reinterpret_cast<const brmq_query*>(batch.data()), batch.size(),
+                                   cfg.block_sizes.data(), uint32_t(cfg.block_sizes.size()), out.data(),
+                                   BRMQ_PTR_HOST));
+    return out;
+}
+
 }  // namespace batchrmq

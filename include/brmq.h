@@ -93,6 +93,16 @@ const char* brmq_last_error(void);
 int brmq_solve_bbst(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
                     uint64_t q, uint32_t k, uint64_t* answers, uint32_t flags);
 
+/* SPEC.md:266-310 solve_batch_bbst(array, batch, LevelConfig{k_1 < ... < k_h})
+ * -- multi-level BbST.  Supported chains: h = 1 ({k}, same as
+ * brmq_solve_bbst) and h = 2 with k_1 = 32 and k_2 a multiple of 32: one pass
+ * over A stores the 32-element sub-block minima next to the k_2-block minima,
+ * and endpoint blocks are resolved through them (raw A is read only inside one
+ * partial sub-block per edge).  Other chains -> BRMQ_EINVAL. */
+int brmq_solve_bbst_ml(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
+                       uint64_t q, const uint32_t* ks, uint32_t h, uint64_t* answers,
+                       uint32_t flags);
+
 /* SPEC.md:237-245 solve_batch_bbst_con(array, batch, BbstConParams{k, sort_kind})
  * -- BbST_CON: endpoint sort, contraction of A into A_Q,
  * block Sparse Table over A_Q, speculative answering. */

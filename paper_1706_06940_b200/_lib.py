@@ -42,6 +42,8 @@ SIGNATURES = {
     "brmq_ctx_stream": (vp, [vp]),
     "brmq_last_error": (C.c_char_p, []),
     "brmq_solve_bbst": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint32, vp, C.c_uint32]),
+    "brmq_solve_bbst_ml": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, C.c_uint32, vp,
+                                     C.c_uint32]),
     "brmq_solve_bbst_con": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint32, C.c_int, vp,
                                       C.c_uint32]),
     "brmq_collect_endpoints": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint32]),

@@ -170,6 +170,10 @@ class Engine:
         """SPEC.md:302-310, BbST with one level."""
         return self._solve(False, array, batch, k, 0, out)
 
+    def solve_batch_bbst_ml(self, array, batch, ks=(32, 512), out=None):
+        """SPEC.md:266-310 with LevelConfig ks (h = 1, or h = 2 with k_1 = 32)."""
+        return self._solve("ml", array, batch, tuple(int(x) for x in ks), 0, out)
+
     def solve_batch_bbst_con(self, array, batch, k: int = 512,
                              sort_kind: SortKind = SortKind.Radix, out=None):
         """SPEC.md:237-245, BbST_CON (PAPER.md:210-272)."""
@@ -191,7 +195,10 @@ class Engine:
             if out is None:
                 out = np.empty(q, dtype=np.uint64)
             a, b, o, flags = _ptr(array), _ptr(batch), _ptr(out), PTR_HOST
-        if con:
+        if con == "ml":
+            ks = (C.c_uint32 * len(k))(*k)
+            rc = self._L.brmq_solve_bbst_ml(self._h, a, n, b, q, ks, len(k), o, flags)
+        elif con:
             rc = self._L.brmq_solve_bbst_con(self._h, a, n, b, q, int(k), sort_kind, o, flags)
         else:
             rc = self._L.brmq_solve_bbst(self._h, a, n, b, q, int(k), o, flags)

@@ -517,6 +517,87 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     return map_err(c->ctl_host->err);
 }
 
+// ------------------------------------------------------------ multi-level BbST
+int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
+                       const uint32_t* ks, uint32_t h, uint64_t* answers, uint32_t flags) {
+    if (!c || !ks) return fail(BRMQ_EINVAL, "null argument");
+    if (h == 1) return brmq_solve_bbst(c, A, n, Q, q, ks[0], answers, flags);
+    if (h != 2 || ks[0] != 32 || ks[1] <= 32 || ks[1] % 32 != 0)
+        return fail(BRMQ_EINVAL,
+                    "solve_batch_bbst: supported level configs are [k] and [32, k] with 32 | k");
+    const uint32_t k = ks[1];
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    c->info.k = k;
+    Timer tm(c);
+    if (q == 0) {
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t b = (n + k - 1) / k;
+    const uint32_t L = brmq::floor_log2_u64(b) + 1;
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_st = cv.add(size_t(L) * b * 8);
+    const size_t i_sub = cv.add(((n + 31) / 32) * 8);
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
+    auto* SUB = reinterpret_cast<uint64_t*>(P(i_sub));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    int launches = 0;
+    auto enqueue = [&]() -> int {
+        int l = 0;
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        tm.stage("block_argmin", launches);
+        l = brmq::launch_block_argmin_ml(dA, n, k, ST, SUB, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("sparse_table", launches);
+        l = brmq::launch_sparse_table(ST, b, nullptr, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("query", launches);
+        l = brmq::launch_query_ml(dA, n, k, ST, b, SUB, dQ, q, dAns, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        return BRMQ_OK;
+    };
+    const GraphKey key{2, A, n, Q, q, k, 32, answers, s};
+    if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    c->info.blocks = b;
+    c->info.levels = L;
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(c->ctl_host->err);
+}
+
 // ------------------------------------------------------------------ BbST_CON
 int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q,
                         uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,

@@ -144,3 +144,97 @@ int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t
 }
 
 }  // namespace brmq
+
+// ---------------------------------------------------------------------------
+// Two-level block minima for multi-level BbST
+// with k1 = 32: besides the k-block keys (level 0 of the Sparse Table) the same
+// single pass over A stores the leftmost-min key of every 32-element sub-block
+// (one 128-byte row), 8 B per 128 B read (+6% traffic).  Vector path: lane l of
+// round u holds 16-byte vector 32u + l of the block, so the 8 lanes of a quarter
+// warp cover one sub-block and reduce it with two masked redux.sync.
+namespace brmq {
+namespace {
+
+__global__ void __launch_bounds__(kThreads) k_block_argmin_ml_vec(const int32_t* __restrict__ A,
+                                                                  uint64_t n, uint64_t nfull,
+                                                                  uint64_t nblk, uint32_t k,
+                                                                  uint64_t* __restrict__ keys,
+                                                                  uint64_t* __restrict__ sub) {
+    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (blk >= nblk) return;
+    const unsigned lane = lane_id();
+    const uint64_t lo = blk * k;
+    if (blk >= nfull) {  // clipped trailing block: sub-block by sub-block, scalar
+        uint64_t best = kNoKey;
+        for (uint64_t sb = lo; sb < n; sb += 32) {
+            const uint64_t i = sb + lane;
+            uint64_t kk = i < n ? pack_key(__ldg(A + i), uint32_t(i)) : kNoKey;
+            kk = warp_min_key(kk);
+            if (lane == 0) sub[sb >> 5] = kk;
+            best = kmin(best, kk);
+        }
+        if (lane == 0) keys[blk] = best;
+        return;
+    }
+    const int4* v4 = reinterpret_cast<const int4*>(A + lo);
+    const uint32_t nvec = k >> 2;  // multiple of 32
+    uint64_t best = kNoKey;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+        int4 x[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (v0 + 32 * u < nvec) x[u] = ld_stream_v4(v4 + v0 + 32 * u + lane);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            const uint32_t p = uint32_t(lo) + 4 * (v0 + 32 * u + lane);
+            int32_t bv = x[u].x;
+            uint32_t bp = p;
+            if (x[u].y < bv) { bv = x[u].y; bp = p + 1; }
+            if (x[u].z < bv) { bv = x[u].z; bp = p + 2; }
+            if (x[u].w < bv) { bv = x[u].w; bp = p + 3; }
+            const uint64_t sk = group_min_key<8>(pack_key(bv, bp));  // the quarter warp's sub-block
+            if ((lane & 7u) == 0) sub[(lo >> 5) + ((v0 + 32 * u + lane) >> 3)] = sk;
+            best = kmin(best, sk);
+        }
+    }
+    best = warp_min_key(best);
+    if (lane == 0) keys[blk] = best;
+}
+
+// any k (multiple of 32) / alignment: sub-block by sub-block with coalesced scalars
+__global__ void __launch_bounds__(kThreads) k_block_argmin_ml_gen(const int32_t* __restrict__ A,
+                                                                  uint64_t n, uint64_t nblk,
+                                                                  uint32_t k,
+                                                                  uint64_t* __restrict__ keys,
+                                                                  uint64_t* __restrict__ sub) {
+    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (blk >= nblk) return;
+    const unsigned lane = lane_id();
+    const uint64_t lo = blk * k, hi = lo + k < n ? lo + k : n;
+    uint64_t best = kNoKey;
+    for (uint64_t sb = lo; sb < hi; sb += 32) {
+        const uint64_t i = sb + lane;
+        uint64_t kk = i < hi ? pack_key(__ldg(A + i), uint32_t(i)) : kNoKey;
+        kk = warp_min_key(kk);
+        if (lane == 0) sub[sb >> 5] = kk;
+        best = kmin(best, kk);
+    }
+    if (lane == 0) keys[blk] = best;
+}
+
+}  // namespace
+
+int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
+                           uint64_t* sub, cudaStream_t stream) {
+    const uint64_t nblk = (n + k - 1) / k;
+    if (nblk == 0) return 0;
+    if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
+        k_block_argmin_ml_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys,
+                                                                            sub);
+    else
+        k_block_argmin_ml_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, nblk, k, keys, sub);
+    return 1;
+}
+
+}  // namespace brmq

@@ -20,6 +20,11 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
 int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
                              uint32_t k, uint64_t* keys, uint64_t* b_dev, cudaStream_t stream);
 
+// Multi-level (k1 = 32) variant: also stores the leftmost-min key of every
+// 32-element sub-block in sub[ceil(n/32)] (k must be a multiple of 32).
+int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
+                           uint64_t* sub, cudaStream_t stream);
+
 // ---------------------------------------------------------------- sparse_table.cu
 // Levels 1..L-1 of the block Sparse Table, row e at ST + e*b (row 0 = level 0).
 // b_dev (nullable) holds the true block count <= b (rows stay strided by b).
@@ -29,6 +34,11 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST,
                         uint64_t b, const uint64_t* Q, uint64_t q, uint64_t* answers,
                         uint32_t* err, cudaStream_t stream);
+// Multi-level BbST [32, k] answering: endpoint blocks resolved through the
+// 32-element sub-block keys, raw A read only inside partial sub-blocks.
+int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
+                    const uint64_t* sub, const uint64_t* Q, uint64_t q, uint64_t* answers,
+                    uint32_t* err, cudaStream_t stream);
 int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint32_t k,
                             const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
                             const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,

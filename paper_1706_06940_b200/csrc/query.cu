@@ -285,3 +285,138 @@ int launch_query_contracted(const uint64_t* AQ, const uint64_t* /*aq_len_dev*/, 
 }
 
 }  // namespace brmq
+
+// ---------------------------------------------------------------------------
+// Multi-level BbST [k1 = 32, k] (SPEC.md:293-296 answer_one_ml).
+// The O(1) part is the same as above; an endpoint block that must be resolved
+// descends to its 32-element sub-blocks: full sub-blocks inside the range come
+// from their stored keys (one 128-byte line per block for k = 512), and raw A
+// is read only for a partial sub-block whose stored minimum lies outside the
+// range -- with the same leftmost-exact speculation (<= on the left, < on the
+// right) one level down.  Each lane resolves its own query: per lane at most
+// two sub-block-key lines and four 128-byte rows, all lanes in parallel, so the
+// warp never serialises on other lanes' scans.
+namespace brmq {
+namespace {
+
+// leftmost-min key of A[lo..hi] inside one 32-aligned row (one 128-byte line)
+template <bool VEC>
+__device__ __forceinline__ uint64_t row_scan(const int32_t* __restrict__ A, uint64_t n, uint64_t lo,
+                                             uint64_t hi) {
+    const uint64_t r0 = lo & ~uint64_t(31);
+    uint64_t best = kNoKey;
+    if (VEC && r0 + 32 <= n) {
+        const int4* v = reinterpret_cast<const int4*>(A + r0);
+        const uint32_t c0 = uint32_t(lo - r0) >> 2, c1 = uint32_t(hi - r0) >> 2;
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c) {
+            if (c < c0 || c > c1) continue;
+            const int4 x = __ldg(v + c);
+            const uint64_t p = r0 + 4 * c;
+            if (p + 0 >= lo && p + 0 <= hi) best = kmin(best, pack_key(x.x, uint32_t(p + 0)));
+            if (p + 1 >= lo && p + 1 <= hi) best = kmin(best, pack_key(x.y, uint32_t(p + 1)));
+            if (p + 2 >= lo && p + 2 <= hi) best = kmin(best, pack_key(x.z, uint32_t(p + 2)));
+            if (p + 3 >= lo && p + 3 <= hi) best = kmin(best, pack_key(x.w, uint32_t(p + 3)));
+        }
+        return best;
+    }
+    for (uint64_t i = lo; i <= hi; ++i) best = kmin(best, pack_key(__ldg(A + i), uint32_t(i)));
+    return best;
+}
+
+// Resolve A[lo..hi] (inside one k-block) against the running best, through the
+// sub-block keys.  A partial sub-block [a, b] whose stored minimum S lies outside
+// it can hold no key below pack(value(S), a), so it is scanned iff that bound is
+// below the running best -- the exact form of the leftmost rule, valid whatever
+// side of the partial range the current best comes from.
+template <bool VEC>
+__device__ __forceinline__ uint64_t resolve_sub(const int32_t* __restrict__ A, uint64_t n,
+                                                const uint64_t* __restrict__ sub, uint64_t lo,
+                                                uint64_t hi, uint64_t best) {
+    const uint64_t sl = lo >> 5, sr = hi >> 5;
+    if (sl == sr) {
+        const uint64_t S = __ldg(sub + sl);
+        if (key_pos(S) >= lo && key_pos(S) <= hi) return kmin(best, S);
+        if ((S & ~0xFFFFFFFFull) + lo >= best) return best;  // bound pack(v(S), lo) not below best
+        return kmin(best, row_scan<VEC>(A, n, lo, hi));
+    }
+    uint64_t inner = kNoKey;
+    for (uint64_t s = sl + 1; s < sr; ++s) inner = kmin(inner, __ldg(sub + s));
+    best = kmin(best, inner);
+    const uint64_t Rk = __ldg(sub + sr), Lk = __ldg(sub + sl);
+    bool scan_r = false, scan_l = false;
+    if (key_pos(Rk) <= hi) best = kmin(best, Rk);
+    else scan_r = true;
+    if (key_pos(Lk) >= lo) best = kmin(best, Lk);
+    else scan_l = true;
+    if (scan_r && (Rk & ~0xFFFFFFFFull) + (sr << 5) < best)
+        best = kmin(best, row_scan<VEC>(A, n, sr << 5, hi));
+    if (scan_l && (Lk & ~0xFFFFFFFFull) + lo < best)
+        best = kmin(best, row_scan<VEC>(A, n, lo, (sl << 5) + 31));
+    return best;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict__ A, uint64_t n,
+                                                       uint32_t k, const uint64_t* __restrict__ ST,
+                                                       uint64_t stride,
+                                                       const uint64_t* __restrict__ sub,
+                                                       const uint64_t* __restrict__ Q, uint64_t q,
+                                                       uint64_t* __restrict__ answers,
+                                                       uint32_t* __restrict__ err) {
+    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+    uint64_t l = x.x, r = x.y;
+    if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
+    if (r >= n) {                                        // naive.hpp:14-15
+        atomicOr(err, 1u);
+        answers[i] = ~0ull;
+        return;
+    }
+    if (l == r) {
+        answers[i] = l;
+        return;
+    }
+    const uint64_t bl = l / k, br = r / k;
+    const uint64_t L = __ldg(ST + bl);
+    uint64_t best = kNoKey;
+    if (bl == br) {
+        best = (key_pos(L) >= l && key_pos(L) <= r) ? L : resolve_sub<VEC>(A, n, sub, l, r, kNoKey);
+    } else {
+        if (br - bl >= 2) {  // inner_span_min
+            const uint32_t e = floor_log2_u64(br - bl - 1);
+            const uint64_t* row = ST + uint64_t(e) * stride;
+            best = kmin(__ldg(row + bl + 1), __ldg(row + br - (1ull << e)));
+        }
+        const uint64_t R = __ldg(ST + br);
+        bool res_r = false, res_l = false;
+        if (best == kNoKey || key_hi(R) < key_hi(best)) {
+            if (key_pos(R) <= r) best = kmin(best, R);
+            else res_r = true;
+        }
+        if (best == kNoKey || key_hi(L) <= key_hi(best)) {
+            if (key_pos(L) >= l) best = kmin(best, L);
+            else res_l = true;
+        }
+        if (res_r) best = resolve_sub<VEC>(A, n, sub, br * k, r, best);
+        if (res_l) best = resolve_sub<VEC>(A, n, sub, l, bl * k + k - 1, best);
+    }
+    answers[i] = key_pos(best);
+}
+
+}  // namespace
+
+int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
+                    const uint64_t* sub, const uint64_t* Q, uint64_t q, uint64_t* answers,
+                    uint32_t* err, cudaStream_t stream) {
+    if (q == 0) return 0;
+    const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
+    if ((reinterpret_cast<uintptr_t>(A) & 15u) == 0)
+        k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err);
+    else
+        k_query_ml<false><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err);
+    return 1;
+}
+
+}  // namespace brmq

@@ -33,6 +33,7 @@ int main() {
     CHECK((solve_batch_bbst_con(A, batch) == Answers{3, 3}));
     CHECK((solve_batch_bbst_con(A, batch, BbstConParams{2, SortKind::Comparison, 4}) == Answers{3, 3}));
     CHECK((solve_batch_bbst(A, batch, 2) == Answers{3, 3}));
+    CHECK((solve_batch_bbst(A, batch, LevelConfig{{32, 64}}) == Answers{3, 3}));
     CHECK(floor_log2(48829) == 15);
     bool thrown = false;
     try {

@@ -14,7 +14,7 @@ from paper_1706_06940_b200 import (ENDPOINT_DTYPE, InvalidArgument, LogicError, 
 pytestmark = pytest.mark.gpu
 
 KS = [1, 2, 3, 7, 8, 64, 128, 256, 512, 1024, 2048, 4096]
-VARIANTS = ["bbst", "con_radix", "con_bitmap"]
+VARIANTS = ["bbst", "bbst_ml", "con_radix", "con_bitmap"]
 
 
 def _values(r, n, kind):
@@ -63,6 +63,10 @@ def _queries(r, n, q, kind):
 def _solve(engine, variant, A, Q, k):
     if variant == "bbst":
         return engine.solve_batch_bbst(A, Q, k)
+    if variant == "bbst_ml":  # multi-level [32, k]; k must be a multiple of 32 above 32
+        if k == 0:
+            return engine.solve_batch_bbst_ml(A, Q, (32, 0))
+        return engine.solve_batch_bbst_ml(A, Q, (32, k if k % 32 == 0 and k > 32 else 512))
     kind = SortKind.Radix if variant == "con_radix" else SortKind.Bitmap
     return engine.solve_batch_bbst_con(A, Q, k, kind)
 
@@ -117,6 +121,24 @@ def test_edge_cases(engine, orc, variant):
     assert list(_solve(engine, variant, A, make_queries([3], [9]), 4)) == [9]
 
 
+def test_multilevel_configs(engine, orc):
+    r = np.random.default_rng(31)
+    A = _values(r, 70_001, "ties16")
+    Q = _queries(r, 70_001, 20_000, "mixed")
+    want = orc.naive_numpy(A, Q)
+    for ks in [(512,), (32, 64), (32, 96), (32, 512), (32, 4096)]:
+        assert np.array_equal(engine.solve_batch_bbst_ml(A, Q, ks), want), ks
+    for bad in [(16, 512), (32, 48), (32, 16), (64, 512), (32, 64, 512)]:
+        with pytest.raises(InvalidArgument):
+            engine.solve_batch_bbst_ml(A, Q, bad)
+    # unaligned device pointer (scalar fallbacks)
+    torch = pytest.importorskip("torch")
+    dA = torch.from_numpy(np.concatenate([[0], A]).astype(np.int32)).cuda()[1:]
+    dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+    assert np.array_equal(engine.solve_batch_bbst_ml(dA, dQ, (32, 512)).cpu().numpy().view(np.uint64), want)
+    assert np.array_equal(engine.solve_batch_bbst(dA, dQ, 512).cpu().numpy().view(np.uint64), want)
+
+
 def test_device_pointers(engine, orc):
     torch = pytest.importorskip("torch")
     r = np.random.default_rng(7)
@@ -128,6 +150,8 @@ def test_device_pointers(engine, orc):
     for variant in VARIANTS:
         if variant == "bbst":
             out = engine.solve_batch_bbst(dA, dQ, 512)
+        elif variant == "bbst_ml":
+            out = engine.solve_batch_bbst_ml(dA, dQ, (32, 512))
         else:
             out = engine.solve_batch_bbst_con(dA, dQ, 512,
                                               SortKind.Radix if variant == "con_radix" else SortKind.Bitmap)

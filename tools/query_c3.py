@@ -9,7 +9,9 @@ for cfg in ('c3', 'c4', 'c5'):
     s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
     dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
-    ms, st, _ = time_solves(eng, torch, s, lambda: eng.solve_batch_bbst(dA, dQ, 512), 3, 1, flush, timing=1)
-    res[cfg] = {k: round(v[0], 4) for k, v in st.items()}
+    for name, f in (('h1', lambda: eng.solve_batch_bbst(dA, dQ, 512)), ('ml', lambda: eng.solve_batch_bbst_ml(dA, dQ, (32, 512)))):
+        ms, _, _ = time_solves(eng, torch, s, f, 5, 2, flush, timing=0)
+        _, st, _ = time_solves(eng, torch, s, f, 3, 1, flush, timing=1)
+        res[cfg + '/' + name] = {'ms': round(statistics.mean(ms), 4), 'qps': Q.shape[0] / statistics.mean(ms) * 1e3, **{k: round(v[0], 4) for k, v in st.items()}}
     del dA, dQ, A, Q; eng.close(); torch.cuda.empty_cache()
-print(json.dumps(res))
+print(json.dumps(res, indent=0))
