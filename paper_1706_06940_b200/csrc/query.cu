@@ -300,8 +300,10 @@ namespace brmq {
 namespace {
 
 // leftmost-min key of A[lo..hi] inside one 32-aligned row (one 128-byte line)
+// Out of line on purpose: one shared copy keeps the kernel inside the
+// instruction cache (the inlined variants thrashed it: "no_instructions" stalls).
 template <bool VEC>
-__device__ __forceinline__ uint64_t row_scan(const int32_t* __restrict__ A, uint64_t n, uint64_t lo,
+__device__ __noinline__ uint64_t row_scan(const int32_t* __restrict__ A, uint64_t n, uint64_t lo,
                                              uint64_t hi) {
     const uint64_t r0 = lo & ~uint64_t(31);
     uint64_t best = kNoKey;
@@ -330,7 +332,7 @@ __device__ __forceinline__ uint64_t row_scan(const int32_t* __restrict__ A, uint
 // below the running best -- the exact form of the leftmost rule, valid whatever
 // side of the partial range the current best comes from.
 template <bool VEC>
-__device__ __forceinline__ uint64_t resolve_sub(const int32_t* __restrict__ A, uint64_t n,
+__device__ __noinline__ uint64_t resolve_sub(const int32_t* __restrict__ A, uint64_t n,
                                                 const uint64_t* __restrict__ sub, uint64_t lo,
                                                 uint64_t hi, uint64_t best) {
     const uint64_t sl = lo >> 5, sr = hi >> 5;
