@@ -367,6 +367,9 @@ def run_ours(args) -> dict:
         rec["cpu_baseline"] = base
     if rank == 0 and args.sweep and world == 1:
         rec["sweep"] = run_sweep(eng, torch, stream, flush, dA, A, args)
+        del dA, dQ, dAns
+        torch.cuda.empty_cache()
+        rec["configs"] = run_configs(eng, torch, stream, flush, args)
     eng.close()
     if dist:
         dist.destroy_process_group()
@@ -396,6 +399,42 @@ def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
             t = statistics.mean(ms)
             out.append({"q": q, "variant": v, "queries_per_s": q / (t * 1e-3), "ms": t,
                         "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}})
+    return out
+
+
+def run_configs(eng, torch, stream, flush, args) -> dict:
+    """Every BASELINE.json configuration at full size, every engine variant, each
+    answer set checked against the reference pipeline (oracle/_ref) on the host."""
+    import oracle
+    out = {}
+    for name in ("c1", "c3", "c4", "c5"):
+        A, Q = gen_workload(name)
+        q = Q.shape[0]
+        t0 = time.perf_counter()
+        want = None if args.no_cpu else oracle.solve_oracle(A, Q)
+        t_cpu = time.perf_counter() - t0
+        dA = torch.from_numpy(A).to("cuda")
+        dQ = torch.from_numpy(Q.view(np.int64)).to("cuda")
+        dO = torch.empty(q, dtype=torch.int64, device="cuda")
+        res = {"n": int(A.shape[0]), "q": q}
+        if want is not None:
+            res["cpu_reference_queries_per_s"] = q / t_cpu
+        variants = {
+            "bbst": lambda: eng.solve_batch_bbst(dA, dQ, 512, out=dO),
+            "bbst_ml_32_512": lambda: eng.solve_batch_bbst_ml(dA, dQ, (32, 512), out=dO),
+            "con_radix": lambda: eng.solve_batch_bbst_con(dA, dQ, 512, 0, out=dO),
+            "con_bitmap": lambda: eng.solve_batch_bbst_con(dA, dQ, 512, 2, out=dO),
+        }
+        for v, f in variants.items():
+            ms, _, _ = time_solves(eng, torch, stream, f, 5, 3, flush, timing=0)
+            _, stages, _ = time_solves(eng, torch, stream, f, 2, 0, flush, timing=1)
+            ok = None if want is None else bool(np.array_equal(dO.cpu().numpy().view(np.uint64), want))
+            t = statistics.mean(ms)
+            res[v] = {"queries_per_s": q / (t * 1e-3), "ms": t, "bit_exact_vs_reference": ok,
+                      "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}}
+        out[name] = res
+        del dA, dQ, dO, A, Q, want
+        torch.cuda.empty_cache()
     return out
 
 
