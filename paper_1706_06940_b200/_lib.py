@@ -7,9 +7,11 @@ raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libbrmq.so"
+# BRMQ_LIB overrides the in-tree library (A/B builds in tools/; never a fallback)
+LIB_PATH = Path(os.environ.get("BRMQ_LIB") or Path(__file__).resolve().parent / "libbrmq.so")
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

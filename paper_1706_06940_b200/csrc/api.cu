@@ -49,6 +49,9 @@ struct Control {
     uint64_t nb;        // |boundary|
     uint64_t aq_len;    // |A_Q|
     uint64_t b_dev;     // blocks over A_Q
+    // boundaries per contraction range (bitmap pipeline) or their exclusive
+    // prefix (radix pipeline / stage API), zeroed with the rest of the block
+    uint32_t rcnt[brmq::kMaxContractRanges + 1];
 };
 
 }  // namespace
@@ -626,6 +629,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const uint32_t L = brmq::floor_log2_u64(b_max) + 1;
     const uint64_t ntiles = brmq::contract_tiles(n);
     const int bits = bits_for(n);
+    uint32_t G = 0, R = 0;
+    brmq::contract_partition(n, &G, &R);
     if (int rc = ensure_bitmap(c, n)) return rc;
 
     Carve cv;
@@ -682,7 +687,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
-            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->span, &ctl->err, s);
+            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->rcnt, R,
+                                     ctl->span, &ctl->err, s);
             launches += l;
             tm.end(l);
         } else {
@@ -691,7 +697,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
             auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
             tm.stage("collect", launches);
-            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s);
+            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s);
             launches += l;
             tm.end(l);
             tm.stage("radix_sort", launches);
@@ -702,13 +708,14 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             tm.end(l);
             tm.stage("unique_rank", launches);
             l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr,
-                                    c->bitmap, ctl->span, &ctl->nb, &ctl->err, S(i_ust),
+                                    c->bitmap, ctl->rcnt, R, ctl->span, &ctl->nb, &ctl->err, S(i_ust),
                                     &ctl->tickets[0], c->epoch_dev, 1, s);
             launches += l;
             tm.end(l);
         }
         tm.stage("contract", launches);
-        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len,
+        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, !use_bitmap, AQ,
+                                  &ctl->nb, &ctl->aq_len,
                                   use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
                                   c->epoch_dev, 0, s);
         launches += l;
@@ -779,7 +786,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
     if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
     auto* v = reinterpret_cast<uint32_t*>(P(i_v));
-    brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
+    brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, 0, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
     brmq::launch_join_eps(k, v, m, dE, s);
     if (int rc = check_status(c)) return rc;
     if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));
@@ -869,7 +876,10 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     if (int rc = begin_epochs(c, 2)) return rc;
     k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, 2);
     c->epoch_host += 2;
-    brmq::launch_unique(k, v, m, n, bd, nullptr, nullptr, c->bitmap, ctl->span, &ctl->nb, &ctl->err,
+    uint32_t G = 0, R = 0;
+    brmq::contract_partition(n, &G, &R);
+    brmq::launch_unique(k, v, m, n, bd, nullptr, nullptr, c->bitmap, ctl->rcnt, R, ctl->span,
+                        &ctl->nb, &ctl->err,
                         S(i_ust), &ctl->tickets[0], c->epoch_dev, 0, s);
     if (int rc = sync_and_read_control(c, ctl)) return rc;
     if (c->ctl_host->err) {
@@ -878,7 +888,8 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         CUDA_TRY(cudaStreamSynchronize(s));
         return map_err(c->ctl_host->err);
     }
-    brmq::launch_contract(dA, n, c->bitmap, ctl->span, AQ, &ctl->nb, &ctl->aq_len, nullptr,
+    brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, true, AQ, &ctl->nb,
+                          &ctl->aq_len, nullptr,
                           S(i_cst), c->epoch_dev, 1, s);
     brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);
     brmq::launch_u32_to_u64(bd, &ctl->nb, m, dbo, s);

@@ -33,14 +33,22 @@ constexpr int kTile = kThreads * kItems;  // 4096
 // ------------------------------------------------------------------ collect
 // span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
 // Grid-stride with a capped grid so the span needs only 2 atomics per CTA.
+// With a bitmap, also counts the distinct positions of every contraction range
+// (range = (pos >> kContractTileLog2) / R) into rcnt[G]: a bit that the
+// atomicOr newly set is a new boundary.  Counted in a shared histogram first,
+// so the global counters see one add per (CTA, range).
 __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restrict__ Q, uint64_t q,
                                                       uint64_t n, uint32_t* __restrict__ keys,
                                                       uint32_t* __restrict__ vals,
                                                       uint32_t* __restrict__ bitmap,
-                                                      uint32_t* __restrict__ span,
+                                                      uint32_t* __restrict__ rcnt, uint32_t R,
+                                                      uint32_t G, uint32_t* __restrict__ span,
                                                       uint32_t* __restrict__ err) {
     __shared__ uint32_t s_lo, s_hi;
+    __shared__ uint32_t s_hist[kMaxContractRanges];
     if (threadIdx.x == 0) { s_lo = 0xFFFFFFFFu; s_hi = 0; }
+    if (bitmap)
+        for (uint32_t j = threadIdx.x; j < G; j += kThreads) s_hist[j] = 0;
     __syncthreads();
     uint32_t lo_acc = 0xFFFFFFFFu, hi_acc = 0;
     const uint64_t stride = uint64_t(gridDim.x) * kThreads;
@@ -60,11 +68,19 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                 make_uint2(uint32_t(i << 1), uint32_t((i << 1) | 1u));  // contraction.hpp:16-18
         }
         if (bitmap) {
-            atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
-            atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
+            const uint32_t bl = 1u << (lo & 31), bh = 1u << (hi & 31);
+            if (!(atomicOr(bitmap + (lo >> 5), bl) & bl))
+                atomicAdd(s_hist + (lo >> kContractTileLog2) / R, 1u);
+            if (!(atomicOr(bitmap + (hi >> 5), bh) & bh))
+                atomicAdd(s_hist + (hi >> kContractTileLog2) / R, 1u);
         }
         lo_acc = lo < lo_acc ? lo : lo_acc;
         hi_acc = hi > hi_acc ? hi : hi_acc;
+    }
+    if (bitmap) {
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < G; j += kThreads)
+            if (s_hist[j]) atomicAdd(rcnt + j, s_hist[j]);
     }
     if (span) {
         const uint32_t wlo = __reduce_min_sync(kFull, lo_acc);
@@ -83,10 +99,15 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
 
 // ------------------------------------------------------------------- unique
 // Sorted endpoints -> ranks.  rank(j) = (#distinct positions among 0..j) - 1.
+// With a bitmap, also rfirst[g] (g = 0..G) = rank of the first boundary at or
+// after the start of contraction range g (= |boundary| past the last one): the
+// head of every range change writes the entries it crosses, so the
+// contraction gets its rank bases without counting.
 __global__ void __launch_bounds__(kThreads) k_unique(
     const uint32_t* __restrict__ pos, const uint32_t* __restrict__ org, uint64_t m, uint64_t n,
     uint32_t* __restrict__ boundary, uint32_t* __restrict__ cleft, uint32_t* __restrict__ cright_raw,
-    uint32_t* __restrict__ bitmap, uint32_t* __restrict__ span, uint64_t* __restrict__ nb_out,
+    uint32_t* __restrict__ bitmap, uint32_t* __restrict__ rfirst, uint32_t R, uint32_t G,
+    uint32_t* __restrict__ span, uint64_t* __restrict__ nb_out,
     uint32_t* __restrict__ err, uint64_t* __restrict__ status, uint32_t* __restrict__ ticket,
     const uint32_t* __restrict__ epoch_dev, uint32_t epoch_off) {
     const uint32_t epoch = *epoch_dev + epoch_off;
@@ -159,8 +180,18 @@ __global__ void __launch_bounds__(kThreads) k_unique(
         if (idx >= m) break;
         if ((heads >> j) & 1u) {
             ++r;
-            if (p[j] >= n) atomicOr(err, 2u);  // position past the array: range error
-            else if (bitmap) atomicOr(bitmap + (p[j] >> 5), 1u << (p[j] & 31));
+            if (p[j] >= n) {
+                atomicOr(err, 2u);  // position past the array: range error
+            } else if (bitmap) {
+                atomicOr(bitmap + (p[j] >> 5), 1u << (p[j] & 31));
+                const uint32_t g = (p[j] >> kContractTileLog2) / R;
+                uint32_t g0 = 0;  // first range not yet covered by an earlier head
+                if (idx > 0) {
+                    const uint32_t pp = j > 0 ? p[j - 1] : __ldg(pos + idx - 1);
+                    g0 = (pp >> kContractTileLog2) / R + 1;
+                }
+                for (uint32_t x = g0; x <= g; ++x) rfirst[x] = uint32_t(r - 1);
+            }
             if (boundary) boundary[r - 1] = p[j];
         }
         if (cleft) {
@@ -172,6 +203,8 @@ __global__ void __launch_bounds__(kThreads) k_unique(
         if (idx == m - 1) {
             *nb_out = r;
             if (span) span[1] = p[j];
+            if (bitmap && p[j] < n)
+                for (uint32_t x = (p[j] >> kContractTileLog2) / R + 1; x <= G; ++x) rfirst[x] = uint32_t(r);
         }
     }
 }
@@ -261,23 +294,32 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 
 // ------------------------------------------------------------------ launchers
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
-                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s) {
+                   uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
+                   uint32_t* err, cudaStream_t s) {
     if (q == 0) return 0;
     const unsigned grid = g256(q) < 148u * 16u ? g256(q) : 148u * 16u;
+    uint32_t G = 0, R = 1;
+    if (bitmap) contract_partition(n, &G, &R);
+    if (bitmap && R != range_tiles) return -1;  // caller and kernel disagree on the partition
     k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
-                                           bitmap, span, err);
+                                           bitmap, rcnt, R, G, span, err);
     return 1;
 }
 
 size_t unique_status_words(uint64_t m) { return (m + kTile - 1) / kTile; }
 
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n, uint32_t* boundary,
-                  uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* span,
-                  uint64_t* nb_out, uint32_t* err, uint64_t* status, uint32_t* ticket,
-                  const uint32_t* epoch_dev, uint32_t epoch_off, cudaStream_t s) {
+                  uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* rfirst,
+                  uint32_t range_tiles, uint32_t* span, uint64_t* nb_out, uint32_t* err,
+                  uint64_t* status, uint32_t* ticket, const uint32_t* epoch_dev,
+                  uint32_t epoch_off, cudaStream_t s) {
     if (m == 0) return 0;
+    uint32_t G = 0, R = 1;
+    if (bitmap) contract_partition(n, &G, &R);
+    if (bitmap && R != range_tiles) return -1;
     k_unique<<<unsigned((m + kTile - 1) / kTile), kThreads, 0, s>>>(
-        pos, org, m, n, boundary, cleft, cright_raw, bitmap, span, nb_out, err, status, ticket, epoch_dev, epoch_off);
+        pos, org, m, n, boundary, cleft, cright_raw, bitmap, rfirst, R, G, span, nb_out, err,
+        status, ticket, epoch_dev, epoch_off);
     return 1;
 }
 

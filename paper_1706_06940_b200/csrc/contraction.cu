@@ -52,6 +52,7 @@ constexpr int NW = NT / 32;         // consumer warps per CTA
 constexpr int NTP = NT + 32;        // + one producer warp issuing the TMA ring
 constexpr int kRow = 32;            // positions per thread = one 128-byte row
 constexpr int kTile = NT * kRow;    // 4096 positions = 16 KB per tile
+static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
 constexpr int kMaxStages = 4;       // TMA ring depth (runtime: ContractArgs::stages)
 constexpr int kDense = 4;           // flagged rows per warp above which rows close per thread
 
@@ -175,7 +176,9 @@ struct ContractArgs {
     uint64_t* nb_out;
     uint64_t* aq_len;
     uint2* word_info;
-    uint64_t* st_count;  // [G] epoch-tagged counts (phase A)
+    const uint32_t* rcnt;  // [G] boundaries per range, or (prefix) [G+1] exclusive prefix
+    uint64_t range_tiles;  // R
+    uint32_t prefix;
     uint64_t* st_part;   // [G] epoch-tagged partial descriptors (phase C)
     uint64_t* key_tail;  // [G]
     const uint32_t* epoch_dev;  // device epoch counter (bumped once per solve)
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
     uint64_t* empties = bars + kMaxStages;                                             // empty[S]
     __shared__ uint64_t s_tk[2][NW];  // double-buffered warp totals of the tile scan
     __shared__ uint32_t s_tf[2][NW], s_tc[2][NW];
-    __shared__ uint32_t s_red[NW + 1];
+    __shared__ uint32_t s_red[NW];
     __shared__ unsigned long long s_base;
     __shared__ uint64_t s_head;  // partial of the area closed by the range's first boundary
     __shared__ unsigned long long s_first_rank;
@@ -207,11 +210,14 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
     if (b0 > blast) return;
     const uint32_t epoch = *c.epoch_dev + c.epoch_off;
     const uint64_t tfirst = b0 / kTile, tlast = blast / kTile;
-    const uint64_t G = gridDim.x, cta = blockIdx.x;
-    const uint64_t R = (tlast - tfirst + G) / G;  // ceil(#tiles / G)
-    const uint64_t ta = tfirst + cta * R;
-    if (ta > tlast) return;  // empty range: never a predecessor of a non-empty one
-    const uint64_t tb = ta + R - 1 < tlast ? ta + R - 1 : tlast;
+    // fixed partition of ALL tiles of A into ranges of R tiles (contract_partition);
+    // a CTA works on its range clipped to the span [b0, blast]
+    const uint64_t cta = blockIdx.x, R = c.range_tiles;
+    const uint64_t ra = cta * R;
+    const uint64_t ta = ra > tfirst ? ra : tfirst;
+    const uint64_t tb = ra + R - 1 < tlast ? ra + R - 1 : tlast;
+    if (ta > tb) return;  // nothing of the span: never waited on by a CTA that has work
+    const uint64_t cfirst = tfirst / R;  // the CTA holding b0
     const uint64_t my_count = tb - ta + 1;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
 
@@ -236,53 +242,34 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
     if (TMA && producer && lane == 0)  // prologue: the first kStages tiles, before phase A
         for (uint64_t i = 0; i < my_count && i < uint64_t(kStages); ++i) issue(i);
 
-    // ---- A: boundaries in the range, published at once; base = sum of predecessors
-    if (c.debug == 2) {
-        if (tid == 0) s_base = 0;
+    // ---- A: rank base = boundaries in all earlier ranges.  The endpoint stage
+    // counted them per range while marking the bitmap (rcnt), so this is one
+    // read of at most G counts from L2 -- no dependence on other CTAs' progress.
+    if (c.prefix) {
+        if (tid == 0) {
+            s_base = __ldg(c.rcnt + cta);
+            if (tb == tlast) {  // the CTA holding the span's last tile publishes the sizes
+                const uint64_t nb = __ldg(c.rcnt + cta + 1);
+                *c.nb_out = nb;
+                *c.aq_len = nb - 1;
+            }
+        }
         __syncthreads();
     } else {
-        const uint4* w4 = reinterpret_cast<const uint4*>(c.bitmap + ta * NT);
-        const uint64_t nvec = my_count * (NT / 4);
-        uint32_t cnt = 0;
-        for (uint64_t j0 = tid; !producer && j0 < nvec; j0 += NT * 8) {  // 8 loads in flight per thread
-            uint4 w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                w[u] = j0 + u * NT < nvec ? __ldg(w4 + j0 + u * NT) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) cnt += __popc(w[u].x) + __popc(w[u].y) + __popc(w[u].z) + __popc(w[u].w);
-        }
-        cnt = __reduce_add_sync(kFull, cnt);
-        if (lane == 0) s_red[warp] = cnt;
+        uint32_t sum = 0;
+        for (uint64_t j = tid; !producer && j < cta; j += NT) sum += __ldg(c.rcnt + j);
+        sum = __reduce_add_sync(kFull, sum);
+        if (lane == 0 && !producer) s_red[warp] = sum;
         __syncthreads();
-        if (warp == 0) {
-            uint32_t tot = lane < NW + 1 ? s_red[lane] : 0;
-            tot = __reduce_add_sync(kFull, tot);
-            if (lane == 0)
-                st_release_u64(c.st_count + cta, status_pack(epoch, kStAggregate, tot != 0, tot));
-            // the counts live inside the status words: relaxed loads suffice, and
-            // 4 independent loads per lane stay in flight (no acquire / L1 flush)
-            uint64_t sum = 0;
-            for (uint64_t j0 = lane; j0 < cta; j0 += 128) {
-                uint64_t sw[4];
+        if (tid == 0) {
+            uint64_t base = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    sw[u] = j0 + 32 * u < cta ? ld_relaxed_u64(c.st_count + j0 + 32 * u) : 0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (j0 + 32 * u >= cta) break;
-                    while (status_state(sw[u], epoch) == kStInvalid)
-                        sw[u] = ld_relaxed_u64(c.st_count + j0 + 32 * u);
-                    sum += status_value(sw[u]);
-                }
-            }
-            sum = warp_sum_u64(sum);
-            if (lane == 0) {
-                s_base = sum;
-                if (tb == tlast) {  // the CTA holding the span's last tile publishes the sizes
-                    *c.nb_out = sum + tot;
-                    *c.aq_len = sum + tot - 1;
-                }
+            for (int w = 0; w < NW; ++w) base += s_red[w];
+            s_base = base;
+            if (tb == tlast) {
+                const uint64_t nb = base + __ldg(c.rcnt + cta);
+                *c.nb_out = nb;
+                *c.aq_len = nb - 1;
             }
         }
         __syncthreads();
@@ -345,6 +332,10 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
                 run = (!GEN && fl == 0) ? row_min<true>(rs, tid, 0, kRow - 1) : row_min<false>(rs, tid, lo, jhi);
             else
                 run = row_min<false>(rg, tid, lo, jhi);
+        }
+        if (fm == 0) {  // nothing of this stage is read again: release it before the barrier
+            __syncwarp();
+            if (TMA && lane == 0) mbar_arrive(&empties[st]);
         }
         uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (fm && !dense) {  // sparse flagged rows: one element per lane
@@ -502,8 +493,10 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
         }
         carry = seg_combine(carry, xt);
         rank_run += ct;
-        __syncwarp();
-        if (TMA && lane == 0) mbar_arrive(&empties[st]);  // this warp is done with the stage
+        if (fm) {
+            __syncwarp();
+            if (TMA && lane == 0) mbar_arrive(&empties[st]);  // this warp is done with the stage
+        }
         if (++st == kStages) { st = 0; phase ^= 1u; }
     };
 
@@ -532,14 +525,15 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
                 const int64_t j = p - int64_t(lane);
                 uint64_t sw = 0, k = kNoKey;
                 bool has = false;
-                if (j >= 0) {
+                const bool live = j >= int64_t(cfirst);  // CTAs before b0's hold nothing
+                if (live) {
                     while (status_state(sw = ld_relaxed_u64(c.st_part + j), epoch) == kStInvalid) {
                     }
                     has = status_flag(sw);
                 }
                 __threadfence();  // acquire: the tails were stored before their descriptors
-                if (j >= 0) k = ld_relaxed_u64(c.key_tail + j);
-                const unsigned hm = __ballot_sync(kFull, has || j < 0);
+                if (live) k = ld_relaxed_u64(c.key_tail + j);
+                const unsigned hm = __ballot_sync(kFull, has || !live);
                 const int g = hm ? __ffs(hm) - 1 : 32;
                 acc = kmin(acc, warp_min_key(int(lane) <= g ? k : kNoKey));
                 done = g < 32;
@@ -551,15 +545,15 @@ __global__ void __launch_bounds__(NTP) k_contract(const __grid_constant__ CUtens
 }
 
 struct ContractLaunch {
-    int grid_tma = 0, grid_ldg = 0;
+    int grid = 0;  // co-resident CTAs of both kernel variants (cooperative launch)
     size_t smem_tma = 0;
     uint32_t stages = 0, debug = 0;
 };
 
 ContractLaunch& contract_cfg() {
     static ContractLaunch cfg;
-    if (cfg.grid_tma == 0) {
-        int dev = 0, sms = 0, per = 0;
+    if (cfg.grid == 0) {
+        int dev = 0, sms = 0, per_tma = 0, per_ldg = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const char* e = getenv("BRMQ_CONTRACT_STAGES");  // tuning knob, default 2
@@ -571,10 +565,13 @@ ContractLaunch& contract_cfg() {
         cfg.smem_tma = 1024 + cfg.stages * (sizeof(Stage) + NT * 4) + 2 * kMaxStages * 8;
         cudaFuncSetAttribute(k_contract<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(cfg.smem_tma));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<true>, NTP, cfg.smem_tma);
-        cfg.grid_tma = sms * (per > 0 ? per : 1);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_contract<false>, NTP, 1024 + 2 * kMaxStages * 8);
-        cfg.grid_ldg = sms * (per > 0 ? per : 1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_tma, k_contract<true>, NTP, cfg.smem_tma);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ldg, k_contract<false>, NTP,
+                                                      1024 + 2 * kMaxStages * 8);
+        int per = per_tma < per_ldg ? per_tma : per_ldg;
+        if (per < 1) per = 1;
+        cfg.grid = sms * per;
+        if (cfg.grid > int(kMaxContractRanges)) cfg.grid = int(kMaxContractRanges);
     }
     return cfg;
 }
@@ -583,17 +580,23 @@ ContractLaunch& contract_cfg() {
 
 size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
 size_t contract_bitmap_words(uint64_t n) { return contract_tiles(n) * NT + 4; }
+size_t contract_status_words() { return size_t(2) * kMaxContractRanges; }  // st_part, key_tail
 
-size_t contract_status_words() {
-    const ContractLaunch& cfg = contract_cfg();
-    const int g = cfg.grid_tma > cfg.grid_ldg ? cfg.grid_tma : cfg.grid_ldg;
-    return size_t(3) * g;  // st_count, st_part, key_tail
+void contract_partition(uint64_t n, uint32_t* G, uint32_t* R) {
+    const uint64_t tiles = contract_tiles(n);
+    uint64_t g = uint64_t(contract_cfg().grid);
+    if (g > tiles) g = tiles;
+    if (g == 0) g = 1;
+    const uint64_t r = (tiles + g - 1) / g;
+    *R = uint32_t(r);
+    *G = uint32_t(tiles ? (tiles + r - 1) / r : 1);
 }
 
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
-                    uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
-                    uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
-                    cudaStream_t s) {
+                    const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out,
+                    uint64_t* aq_len,
+                    uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
+                    uint32_t epoch_off, cudaStream_t s) {
     if (n == 0) return 0;
     const ContractLaunch& cfg = contract_cfg();
     CUtensorMap tmap;
@@ -602,17 +605,15 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     // TMA needs a 16-byte aligned base; arrays without a full row use the plain path
     const bool tma = (reinterpret_cast<uintptr_t>(A) & 15u) == 0 && rows > 0 &&
                      make_tmap_rows128(&tmap, A, rows, NT);
-    const uint64_t tiles = contract_tiles(n);
-    int grid = tma ? cfg.grid_tma : cfg.grid_ldg;
-    if (uint64_t(grid) > tiles) grid = int(tiles);
-    const int gmax = int(contract_status_words() / 3);
+    uint32_t G = 0, R = 0;
+    contract_partition(n, &G, &R);
     ContractArgs args{A, n, tma ? rows : 0, bitmap, span, aq, nb_out, aq_len, word_info,
-                      status, status + gmax, status + 2 * gmax, epoch_dev, epoch_off, cfg.stages,
-                      cfg.debug};
+                      rcnt, R, prefix ? 1u : 0u, status, status + kMaxContractRanges, epoch_dev, epoch_off,
+                      cfg.stages, cfg.debug};
     void* params[] = {&tmap, &args};
     cudaLaunchCooperativeKernel(tma ? reinterpret_cast<const void*>(k_contract<true>)
                                     : reinterpret_cast<const void*>(k_contract<false>),
-                                dim3(grid), dim3(NTP), params,
+                                dim3(G), dim3(NTP), params,
                                 tma ? cfg.smem_tma : 1024 + 2 * kMaxStages * 8, s);
     return 1;  // launch errors surface through the caller's cudaGetLastError
 }

@@ -56,12 +56,21 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
                       bool* result_in_alt, const uint32_t* epoch_dev, uint32_t epoch_off);
 
 // ---------------------------------------------------------------- contract.cu
+// The contraction partitions the tiles of A into G ranges of R tiles
+// (contract_partition); the endpoint stage counts the distinct boundaries of
+// each range into rcnt[G] (zeroed by the caller) while it marks the bitmap
+// (k_collect), or -- from sorted endpoints (k_unique) -- writes the exclusive
+// prefix rfirst[0..G] directly; launch_contract's `prefix` says which.
+constexpr uint32_t kMaxContractRanges = 2048;
+constexpr int kContractTileLog2 = 12;  // 4096-position tiles
+void contract_partition(uint64_t n, uint32_t* G, uint32_t* R);
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
-                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s);
+                   uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
+                   uint32_t* err, cudaStream_t s);
 size_t unique_status_words(uint64_t m);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
-                  uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
+                  uint32_t* rcnt, uint32_t range_tiles, uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
                   uint32_t* ticket, const uint32_t* epoch_dev, uint32_t epoch_off, cudaStream_t s);
 size_t contract_tiles(uint64_t n);  // 8192-element tiles over A
 size_t contract_bitmap_words(uint64_t n);  // bitmap words the contraction reads (whole tiles)
@@ -70,7 +79,7 @@ size_t contract_status_words();    // status-arena words the contraction needs
 // packed A_Q keys, |boundary| (nb_out) and |A_Q|; word_info (nullable) gets
 // (rank prefix, bits) of every non-empty bitmap word, which is cleared.
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
-                    uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
+                    const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
                     cudaStream_t s);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
