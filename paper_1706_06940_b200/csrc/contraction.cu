@@ -49,7 +49,7 @@
 namespace brmq {
 namespace {
 
-constexpr int NW = 4;               // warps per CTA, one stream each
+constexpr int NW = 8;               // warps per CTA, one stream each (2 CTAs per SM at 128 registers)
 constexpr int NT = NW * 32;
 constexpr int kRow = 32;            // positions per lane = one 128-byte row
 constexpr int kWTile = 32 * kRow;   // 1024 positions = 4 KB per warp tile
