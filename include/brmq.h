@@ -62,7 +62,8 @@ enum brmq_status {
     BRMQ_EINVAL = 3,  /* std::invalid_argument (contraction.cpp:15,123; est.cpp:11,13,36) */
     BRMQ_ELOGIC = 4,  /* std::logic_error     (contraction.cpp:159,183)                */
     BRMQ_ECUDA = 5,   /* CUDA runtime failure (no reference equivalent)               */
-    BRMQ_ENOMEM = 6   /* std::bad_alloc / cudaErrorMemoryAllocation                   */
+    BRMQ_ENOMEM = 6,  /* std::bad_alloc / cudaErrorMemoryAllocation                   */
+    BRMQ_EIO = 7      /* harness file I/O (brmq_harness.h; no reference equivalent)   */
 };
 
 enum brmq_flags {

@@ -69,6 +69,17 @@ SIGNATURES = {
     "brmq_workload_array": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint]),
     "brmq_workload_queries": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint]),
     "brmq_workload_mix64": (C.c_uint64, [C.c_uint64]),
+    # include/brmq_harness.h
+    "brmq_account_memory": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, u32p, C.c_uint32, u64p,
+                                      C.POINTER(C.c_double)]),
+    "brmq_answers_checksum": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, u64p]),
+    "brmq_write_array_file": (C.c_int, [C.c_char_p, vp, C.c_uint64]),
+    "brmq_read_array_file": (C.c_int, [C.c_char_p, vp, C.c_uint64, u64p]),
+    "brmq_write_query_file": (C.c_int, [C.c_char_p, vp, C.c_uint64]),
+    "brmq_read_query_file": (C.c_int, [C.c_char_p, vp, C.c_uint64, u64p]),
+    "brmq_write_answer_file": (C.c_int, [C.c_char_p, vp, C.c_uint64]),
+    "brmq_read_answer_file": (C.c_int, [C.c_char_p, vp, C.c_uint64, u64p]),
+    "brmq_verify_answers": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, vp, C.c_uint, u64p, u64p]),
 }
 
 _lib = None

@@ -70,7 +70,7 @@ class CudaError(BrmqError, RuntimeError):
 
 
 _CODES = {1: DomainError, 2: OutOfRange, 3: InvalidArgument, 4: LogicError, 5: CudaError,
-          6: MemoryError}
+          6: MemoryError, 7: OSError}
 
 
 def _check(rc: int) -> None:

@@ -14,6 +14,7 @@
 
 #include "../../include/brmq.h"
 #include "common.cuh"
+#include "errors.h"
 #include "kernels.h"
 
 namespace {
@@ -29,6 +30,15 @@ int fail(int code, const char* fmt, ...) {
     g_last_error = buf;
     return code;
 }
+
+}  // namespace
+
+int brmq::set_error(int code, const char* msg) {
+    g_last_error = msg;
+    return code;
+}
+
+namespace {
 
 #define CUDA_TRY(expr)                                                                      \
     do {                                                                                    \
