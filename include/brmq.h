@@ -111,6 +111,13 @@ int brmq_solve_bbst_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_
                         uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
                         uint32_t flags);
 
+/* SPEC.md:331-377 solve_batch_st_rmq_con(array, batch) -- the comparison baseline
+ * ST-RMQ_CON of Alzamel et al. (section 2): marked contraction of A
+ * into <= 4q + 1 entries, element Sparse Table over them, two probes per query.
+ * The endpoint sort is the LSD radix sort. */
+int brmq_solve_st_rmq_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
+                          uint64_t q, uint64_t* answers, uint32_t flags);
+
 /* ------------------------------------------------ stage-level entry points */
 
 /* contraction.hpp:51 collect_endpoints (contraction.cpp:13-23): eps gets 2q

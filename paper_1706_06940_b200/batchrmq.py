@@ -179,7 +179,11 @@ class Engine:
         """SPEC.md:237-245, BbST_CON (PAPER.md:210-272)."""
         return self._solve(True, array, batch, k, int(sort_kind), out)
 
-    def _solve(self, con: bool, array, batch, k: int, sort_kind: int, out):
+    def solve_batch_st_rmq_con(self, array, batch, out=None):
+        """SPEC.md:331-377, the ST-RMQ_CON baseline (section 2)."""
+        return self._solve("st", array, batch, 1, 0, out)
+
+    def _solve(self, con, array, batch, k, sort_kind: int, out):
         if _is_cuda_tensor(array):  # device-resident inputs (torch CUDA tensors)
             import torch
             assert array.dtype == torch.int32 and array.is_contiguous()
@@ -195,7 +199,9 @@ class Engine:
             if out is None:
                 out = np.empty(q, dtype=np.uint64)
             a, b, o, flags = _ptr(array), _ptr(batch), _ptr(out), PTR_HOST
-        if con == "ml":
+        if con == "st":
+            rc = self._L.brmq_solve_st_rmq_con(self._h, a, n, b, q, o, flags)
+        elif con == "ml":
             ks = (C.c_uint32 * len(k))(*k)
             rc = self._L.brmq_solve_bbst_ml(self._h, a, n, b, q, ks, len(k), o, flags)
         elif con:
@@ -279,6 +285,10 @@ def solve_batch_bbst(array, batch, k: int = 512):
 
 def solve_batch_bbst_con(array, batch, k: int = 512, sort_kind: SortKind = SortKind.Radix):
     return default_engine().solve_batch_bbst_con(array, batch, k, sort_kind)
+
+
+def solve_batch_st_rmq_con(array, batch):
+    return default_engine().solve_batch_st_rmq_con(array, batch)
 
 
 def collect_endpoints(batch):

@@ -772,6 +772,139 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     return map_err(h.err);
 }
 
+// ------------------------------------------------------------------ ST-RMQ_CON
+// SPEC.md "baseline" (Alzamel et al., section 2): marked contraction of A
+// into E (each marked position verbatim, each maximal unmarked run by its
+// minimum: 2m + 1 <= 4q + 1 entries; an empty run keeps its slot as +inf, a
+// documented departure from "exactly one entry per run"), an element Sparse
+// Table over E, two probes per query.  Endpoint sort: the LSD radix sort.
+int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q,
+                          uint64_t q, uint64_t* answers, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    c->info.k = 1;
+    Timer tm(c);
+    if (q == 0) {
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t m = 2 * q;
+    const uint64_t e_max = 2 * m + 1;  // |E| <= 4q + 1
+    const uint32_t L = brmq::floor_log2_u64(e_max) + 1;
+    const int bits = bits_for(n);
+    uint32_t G = 0, R = 0;
+    brmq::contract_partition(n, &G, &R);
+    if (int rc = ensure_bitmap(c, n)) return rc;
+
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_cl = cv.add(q * 4);
+    const size_t i_cr = cv.add(q * 4);
+    const size_t i_bd = cv.add(m * 4);
+    const size_t i_st = cv.add(size_t(L) * e_max * 8);  // row 0 = E
+    const size_t i_k0 = cv.add(m * 4), i_v0 = cv.add(m * 4), i_k1 = cv.add(m * 4), i_v1 = cv.add(m * 4);
+    const size_t i_rs = cv.add(brmq::radix_sort_temp_bytes(m, bits));
+    Carve sv;
+    const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
+    const size_t i_rst = sv.add(brmq::radix_sort_status_words(m, bits) * 8);
+    const size_t i_ust = sv.add(brmq::unique_status_words(m) * 8);
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    if (int rc = ensure_status(c, sv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto S = [&](size_t i) { return reinterpret_cast<uint64_t*>(c->st + sv.off[i]); };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    auto* cl = reinterpret_cast<uint32_t*>(P(i_cl));
+    auto* cr = reinterpret_cast<uint32_t*>(P(i_cr));
+    auto* bd = reinterpret_cast<uint32_t*>(P(i_bd));
+    auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    const uint32_t n_epochs = 2u + uint32_t(brmq::radix_sort_passes(bits));
+    if (int rc = begin_epochs(c, n_epochs)) return rc;
+    int launches = 0;
+    auto enqueue = [&]() -> int {
+        int l = 0;
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, n_epochs);
+        launches += 1;
+        auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
+        auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
+        auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
+        auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
+        tm.stage("collect", launches);
+        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("radix_sort", launches);
+        bool in_alt = false;
+        l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), S(i_rst), s, &in_alt,
+                                    c->epoch_dev, 2);
+        launches += l;
+        tm.end(l);
+        tm.stage("unique_rank", launches);
+        l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, bd, cl, cr, c->bitmap,
+                                ctl->rcnt, R, ctl->span, &ctl->nb, &ctl->err, S(i_ust),
+                                &ctl->tickets[0], c->epoch_dev, 1, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("contract", launches);
+        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, true, ST, &ctl->nb,
+                                  &ctl->aq_len, nullptr, S(i_cst), c->epoch_dev, 0, s,
+                                  /*marked=*/true);
+        l += brmq::launch_marked_fill(dA, bd, &ctl->nb, m, ST, s);
+        l += brmq::launch_marked_edges(dA, n, ctl->span, &ctl->nb, ST, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("sparse_table", launches);
+        l = brmq::launch_sparse_table(ST, e_max, &ctl->aq_len, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("query", launches);
+        l = brmq::launch_query_st(dQ, cl, cr, q, ST, e_max, dAns, s);
+        launches += l;
+        tm.end(l);
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        return BRMQ_OK;
+    };
+    const GraphKey key{3, A, n, Q, q, 1, 0, answers, s};
+    if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->epoch_host += n_epochs;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    const Control& h = *c->ctl_host;
+    c->info.boundary = h.nb;
+    c->info.span_lo = ~h.span[0];
+    c->info.span_hi = h.span[1];
+    c->info.blocks = h.aq_len;  // |E|: the element table's columns
+    c->info.levels = h.aq_len ? brmq::floor_log2_u64(h.aq_len) + 1 : 0;
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(h.err);
+}
+
 // ------------------------------------------------------------ stage entry points
 int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_endpoint* eps,
                            uint32_t flags) {

@@ -288,6 +288,74 @@ __global__ void k_keys_to_pos(uint64_t* __restrict__ t, uint64_t count) {
     if (i < count) t[i] = t[i] == kNoKey ? ~0ull : uint64_t(key_pos(t[i]));
 }
 
+// ------------------------------------------------ ST-RMQ_CON (SPEC.md "baseline")
+// Marked contraction E: E[2t+1] = A[b_t] (every marked
+// position verbatim), E[2t] = the unmarked run between b_{t-1} and b_t, E[0] /
+// E[2m] the runs before b_0 / after b_{m-1}.  The contraction kernel in MARKED
+// mode wrote E[2t] as the leftmost minimum of [b_{t-1}, b_t] with both marks read
+// as +inf; when that minimum landed on the mark b_{t-1} the run is empty (no
+// entry: +inf) or all +inf (its first position).
+__global__ void k_marked_fill(const int32_t* __restrict__ A, const uint32_t* __restrict__ bnd,
+                              const uint64_t* __restrict__ m_dev, uint64_t* __restrict__ E) {
+    const uint64_t m = *m_dev;
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const uint32_t b = bnd[t];
+    E[2 * t + 1] = pack_key(__ldg(A + b), b);
+    if (t == 0) {
+        E[0] = kNoKey;
+        E[2 * m] = kNoKey;
+    } else {
+        const uint32_t p = bnd[t - 1];
+        const uint64_t x = E[2 * t];
+        if (x == kNoKey || key_pos(x) == p) E[2 * t] = b - p >= 2 ? pack_key(0x7FFFFFFF, p + 1) : kNoKey;
+    }
+}
+
+// E[0] = leftmost minimum of A[0, b_0), E[2m] = of A(b_{m-1}, n): grid-stride,
+// warp reductions, one 64-bit atomicMin per warp and side.
+__global__ void k_marked_edges(const int32_t* __restrict__ A, uint64_t n,
+                               const uint32_t* __restrict__ span, const uint64_t* __restrict__ m_dev,
+                               uint64_t* __restrict__ E) {
+    const uint32_t b0 = ~span[0], blast = span[1];
+    if (b0 > blast) return;
+    const uint64_t pre = b0, suf = n - 1 - blast;  // lengths
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    uint64_t kp = kNoKey, ks = kNoKey;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pre + suf; i += stride) {
+        const uint64_t p = i < pre ? i : blast + 1 + (i - pre);
+        const uint64_t k = pack_key(__ldg(A + p), uint32_t(p));
+        if (i < pre) kp = kmin(kp, k);
+        else ks = kmin(ks, k);
+    }
+    kp = warp_min_key(kp);
+    ks = warp_min_key(ks);
+    if (lane_id() == 0) {
+        if (kp != kNoKey) atomicMin(reinterpret_cast<unsigned long long*>(E), kp);
+        if (ks != kNoKey) atomicMin(reinterpret_cast<unsigned long long*>(E + 2 * *m_dev), ks);
+    }
+}
+
+// Query i: [2 cl + 1, 2 cr + 1] in E through the element Sparse Table (row e at
+// ST + e * stride), the two-range trick of element_sparse_table.cpp:35-44.
+__global__ void k_query_st(const ulonglong2* __restrict__ Q, const uint32_t* __restrict__ cleft,
+                           const uint32_t* __restrict__ cright_raw, uint64_t q,
+                           const uint64_t* __restrict__ ST, uint64_t stride,
+                           uint64_t* __restrict__ answers) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(Q + i);
+    const uint64_t l = x.x < x.y ? x.x : x.y;
+    const uint64_t il = 2 * uint64_t(__ldg(cleft + i)) + 1, ir = 2 * uint64_t(__ldg(cright_raw + i)) + 1;
+    if (il == ir) {  // l == r
+        answers[i] = l;
+        return;
+    }
+    const uint32_t e = floor_log2_u64(ir - il + 1);
+    const uint64_t* row = ST + uint64_t(e) * stride;
+    answers[i] = key_pos(kmin(__ldg(row + il), __ldg(row + ir + 1 - (1ull << e))));
+}
+
 inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 
 }  // namespace
@@ -368,6 +436,30 @@ int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
     }
     return l;
 }
+int launch_marked_fill(const int32_t* A, const uint32_t* boundary, const uint64_t* m_dev,
+                       uint64_t m_max, uint64_t* E, cudaStream_t s) {
+    if (!m_max) return 0;
+    k_marked_fill<<<g256(m_max), 256, 0, s>>>(A, boundary, m_dev, E);
+    return 1;
+}
+
+int launch_marked_edges(const int32_t* A, uint64_t n, const uint32_t* span, const uint64_t* m_dev,
+                        uint64_t* E, cudaStream_t s) {
+    if (!n) return 0;
+    const uint64_t g = (n + 255) / 256;
+    k_marked_edges<<<unsigned(g < 148 * 8 ? g : 148 * 8), 256, 0, s>>>(A, n, span, m_dev, E);
+    return 1;
+}
+
+int launch_query_st(const uint64_t* Q, const uint32_t* cleft, const uint32_t* cright_raw,
+                    uint64_t q, const uint64_t* ST, uint64_t stride, uint64_t* answers,
+                    cudaStream_t s) {
+    if (!q) return 0;
+    k_query_st<<<g256(q), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), cleft, cright_raw,
+                                        q, ST, stride, answers);
+    return 1;
+}
+
 int launch_keys_to_pos(uint64_t* t, uint64_t count, cudaStream_t s) {
     if (!count) return 0;
     k_keys_to_pos<<<g256(count), 256, 0, s>>>(t, count);

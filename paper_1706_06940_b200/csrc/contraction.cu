@@ -57,35 +57,34 @@ constexpr int kTile = 4 * kWTile;   // 4096: the partition unit
 static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
 constexpr int kDense = 4;           // flagged rows per warp tile above which rows close per lane
 
-// Rows of the current tile.  In SMEM mode they come from the warp's swizzled rows
-// (16-byte chunk c of row r at byte r*128 + ((c ^ (r & 7)) << 4)) with explicit
-// shared loads; otherwise (array tail past the tensor map, unaligned A) from
-// global memory, bounded by n.
-template <bool SMEM>
+// Rows of the current warp tile in the warp's swizzled shared rows (16-byte
+// chunk c of row r at byte r*128 + ((c ^ (r & 7)) << 4)), read with explicit
+// shared loads.
 struct Rows {
-    uint32_t stage;  // shared address of the stage
-    const int32_t* g;
-    uint64_t tile_lo, n;
+    uint32_t stage;  // shared address of the warp's rows
+    uint64_t tile_lo;
     __device__ __forceinline__ int4 chunk(uint32_t r, int c) const {
-        if (SMEM) return lds128(stage + r * 128u + ((uint32_t(c) ^ (r & 7u)) << 4));
-        const uint64_t q = tile_lo + uint64_t(r) * kRow + 4 * c;
-        int4 y;
-        y.x = q + 0 < n ? __ldg(g + q + 0) : 0;
-        y.y = q + 1 < n ? __ldg(g + q + 1) : 0;
-        y.z = q + 2 < n ? __ldg(g + q + 2) : 0;
-        y.w = q + 3 < n ? __ldg(g + q + 3) : 0;
-        return y;
+        return lds128(stage + r * 128u + ((uint32_t(c) ^ (r & 7u)) << 4));
     }
     __device__ __forceinline__ int32_t elem(uint32_t r, int j) const {
-        if (SMEM)
-            return lds32(stage + r * 128u + (((uint32_t(j) >> 2) ^ (r & 7u)) << 4) + ((j & 3) << 2));
-        const uint64_t q = tile_lo + uint64_t(r) * kRow + j;
-        return q < n ? __ldg(g + q) : 0;
+        return lds32(stage + elem_offset(r, j));
     }
     __device__ __forceinline__ uint64_t pos(uint32_t r, int j) const {
         return tile_lo + uint64_t(r) * kRow + j;
     }
+    static __device__ __forceinline__ uint32_t elem_offset(uint32_t r, int j) {
+        return r * 128u + (((uint32_t(j) >> 2) ^ (r & 7u)) << 4) + ((j & 3) << 2);
+    }
 };
+
+// A_Q slot of area `idx` (closed by the boundary of rank idx + 1).  BbST_CON:
+// slot idx.  ST-RMQ_CON's marked contraction (SPEC.md "baseline"): entry 2t+1
+// is the marked position b_t itself and entry 2t the unmarked run between
+// b_{t-1} and b_t, so area idx (the run before b_{idx+1}) goes to 2 idx + 2.
+template <bool MARKED>
+__device__ __forceinline__ uint64_t aq_slot(uint64_t idx) {
+    return MARKED ? 2 * idx + 2 : idx;
+}
 
 __device__ __forceinline__ int32_t comp(const int4& x, int e) {
     return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
@@ -131,7 +130,7 @@ __device__ __forceinline__ uint64_t row_min(const RW& rw, uint32_t r, int lo, in
 // Per-thread closing of the areas whose right boundary (bit of fl) lies in
 // [lo, hi] of row r; `cur` = open-segment key entering lo, `rank` =
 // boundaries before.  Used when boundaries are dense.
-template <class RW>
+template <bool MARKED, class RW>
 __device__ __forceinline__ void row_close_areas(const RW& rw, uint32_t r, uint32_t fl, int lo,
                                                 int hi, uint64_t cur, uint64_t rank,
                                                 uint64_t* __restrict__ aq) {
@@ -150,7 +149,7 @@ __device__ __forceinline__ void row_close_areas(const RW& rw, uint32_t r, uint32
                 uint64_t k = cur;
                 if (ri >= 0) k = kmin(k, pack_key(rv, uint32_t(rw.pos(r, ri))));
                 k = kmin(k, pack_key(v, uint32_t(rw.pos(r, j))));  // inclusive right end
-                if (rank > 0) aq[rank - 1] = k;
+                if (rank > 0) aq[aq_slot<MARKED>(rank - 1)] = k;
                 ++rank;
                 cur = kNoKey;
                 rv = v;  // the boundary element opens the next area
@@ -181,7 +180,9 @@ struct ContractArgs {
     uint32_t epoch_off;
 };
 
-template <bool VEC>
+// MARKED: ST-RMQ_CON's marked contraction -- marked positions read as +inf
+// inside the areas (they get their own entries) and areas go to aq_slot.
+template <bool VEC, bool MARKED>
 __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ ContractArgs c) {
     __shared__ __align__(128) int4 s_rows[NW][kWTile / 4];  // per warp: 32 rows x 128 B, swizzled
     __shared__ uint32_t s_cnt[NW];
@@ -224,19 +225,33 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             const int4* A4 = reinterpret_cast<const int4*>(c.A + tile_lo);
 #pragma unroll
             for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(A4 + u * 32 + lane);
+        } else {  // array tail / unaligned A: scalar loads, positions >= n read as 0 (masked later)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t p = tile_lo + 128u * u + 4u * lane;
+                y[u].x = p + 0 < c.n ? __ldg(c.A + p + 0) : 0;
+                y[u].y = p + 1 < c.n ? __ldg(c.A + p + 1) : 0;
+                y[u].z = p + 2 < c.n ? __ldg(c.A + p + 2) : 0;
+                y[u].w = p + 3 < c.n ? __ldg(c.A + p + 3) : 0;
+            }
         }
         fy = c.bitmap[(wa + i) * 32 + lane];
     };
-    auto stage = [&](uint64_t i) {
-        const uint64_t tile_lo = (wa + i) * kWTile;
-        if (VEC && tile_lo + kWTile <= c.n) {
+    auto stage = [&]() {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t row = 4u * u + (lane >> 3), ch = lane & 7u;
-                s_rows[warp][row * 8u + (ch ^ (row & 7u))] = y[u];
-            }
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t row = 4u * u + (lane >> 3), ch = lane & 7u;
+            s_rows[warp][row * 8u + (ch ^ (row & 7u))] = y[u];
         }
         __syncwarp();
+        if (MARKED && fy) {  // marked positions of the lane's row read as +inf
+            const uint32_t base = smem_u32(s_rows[warp]);
+            for (uint32_t m = fy; m; m &= m - 1) {
+                const uint32_t off = Rows::elem_offset(lane, __ffs(m) - 1);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(base + off), "r"(0x7FFFFFFF) : "memory");
+            }
+        }
+        if (MARKED) __syncwarp();
     };
     if (cnt) fetch(0);
 
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
 #pragma unroll
                 for (int w = 0; w < NW; ++w) nb += s_cnt[w];
                 *c.nb_out = nb;
-                *c.aq_len = nb - 1;
+                *c.aq_len = MARKED ? 2 * nb + 1 : nb - 1;
             }
         }
         __syncthreads();
@@ -294,7 +309,6 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         constexpr bool GEN = decltype(gen_tag)::value;
         const uint64_t t = wa + i;
         const uint64_t tile_lo = t * kWTile;
-        const bool smem_rows = VEC && tile_lo + kWTile <= c.n;
         const uint64_t p0 = tile_lo + uint64_t(lane) * kRow;
         int jlo = 0, jhi = kRow - 1;
         bool any = true;
@@ -303,8 +317,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             jlo = p0 >= b0 ? 0 : int(b0 - p0);
             jhi = p0 + kRow - 1 <= blast ? kRow - 1 : int(int64_t(blast) - int64_t(p0));
         }
-        const Rows<true> rs{smem_u32(s_rows[warp]), c.A, tile_lo, c.n};
-        const Rows<false> rg{0, c.A, tile_lo, c.n};
+        const Rows rs{smem_u32(s_rows[warp]), tile_lo};
         const unsigned fm = __ballot_sync(kFull, fl != 0);
 
         if (fm == 0) {  // no boundary in the warp tile: one leftmost minimum
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
                 key = pack_key(wv, uint32_t(rs.pos(uint32_t(L), e)));
             } else {
                 uint64_t run = kNoKey;
-                if (any) run = smem_rows ? row_min<false>(rs, lane, jlo, jhi) : row_min<false>(rg, lane, jlo, jhi);
+                if (any) run = row_min<false>(rs, lane, jlo, jhi);
                 key = warp_min_key(run);
             }
             carry.k = kmin(carry.k, key);
@@ -337,10 +350,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         uint64_t run = kNoKey;
         if (any && (fl == 0 || dense)) {
             const int lo = fl ? 31 - __clz(fl) : jlo;
-            if (!GEN || smem_rows)
-                run = (!GEN && fl == 0) ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, lo, jhi);
-            else
-                run = row_min<false>(rg, lane, lo, jhi);
+            run = (!GEN && fl == 0) ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, lo, jhi);
         }
         uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (!dense) {  // sparse flagged rows: one element per lane
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
                 const int jl = __shfl_sync(kFull, jlo, s);
                 const int jh = __shfl_sync(kFull, jhi, s);
                 const int lo = 31 - __clz(ft);
-                const int32_t v = (!GEN || smem_rows) ? rs.elem(uint32_t(s), int(lane)) : rg.elem(uint32_t(s), int(lane));
+                const int32_t v = rs.elem(uint32_t(s), int(lane));
                 const uint64_t key = pack_key(v, uint32_t(rs.pos(uint32_t(s), int(lane))));
                 const uint64_t mk = warp_min_key(int(lane) >= lo && int(lane) <= jh ? key : kNoKey);
                 if ((ft & (ft - 1)) == 0) {  // one boundary: its head part now, no scan later
@@ -392,17 +402,14 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
                 const SegMin in = seg_combine(carry, we);
                 const uint64_t rank = rank_run + wce;
                 my_rank = rank;
-                auto close = [&](const auto& rw) {
-                    if (in.f) {
-                        row_close_areas(rw, lane, fl, jlo, jhi, in.k, rank, c.aq);
-                    } else {  // first boundary of the piece: its area opened in an earlier piece
-                        const int f = __ffs(fl) - 1;
-                        head = kmin(in.k, row_min<false>(rw, lane, jlo, f));
-                        head_set = true;
-                        row_close_areas(rw, lane, fl & (fl - 1), f, jhi, kNoKey, rank + 1, c.aq);
-                    }
-                };
-                if (!GEN || smem_rows) close(rs); else close(rg);
+                if (in.f) {
+                    row_close_areas<MARKED>(rs, lane, fl, jlo, jhi, in.k, rank, c.aq);
+                } else {  // first boundary of the piece: its area opened in an earlier piece
+                    const int f = __ffs(fl) - 1;
+                    head = kmin(in.k, row_min<false>(rs, lane, jlo, f));
+                    head_set = true;
+                    row_close_areas<MARKED>(rs, lane, fl & (fl - 1), f, jhi, kNoKey, rank + 1, c.aq);
+                }
             }
         } else {
             const int L = 31 - __clz(fm);
@@ -425,14 +432,14 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
                             head = val;
                             head_set = true;
                         } else {
-                            c.aq[rank - 1] = val;
+                            c.aq[aq_slot<MARKED>(rank - 1)] = val;
                         }
                     }
                     continue;
                 }
                 const int jl = __shfl_sync(kFull, jlo, s);
                 const int jh = __shfl_sync(kFull, jhi, s);
-                const int32_t v = (!GEN || smem_rows) ? rs.elem(uint32_t(s), int(lane)) : rg.elem(uint32_t(s), int(lane));
+                const int32_t v = rs.elem(uint32_t(s), int(lane));
                 const bool inr = int(lane) >= jl && int(lane) <= jh;
                 const uint64_t key = inr ? pack_key(v, uint32_t(rs.pos(uint32_t(s), int(lane)))) : kNoKey;
                 const bool isf = (ft >> lane) & 1u;
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
                         head = val;
                         head_set = true;
                     } else if (rk > 0) {
-                        c.aq[rk - 1] = val;
+                        c.aq[aq_slot<MARKED>(rk - 1)] = val;
                     }
                 }
             }
@@ -469,17 +476,16 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         rank_run += wc;
     };
 
-    if (cnt) stage(0);
+    if (cnt) stage();
     for (uint64_t i = 0; i < cnt; ++i) {
         const uint32_t fl = fy;
         if (i + 1 < cnt) fetch(i + 1);  // in flight while tile i is reduced
         const uint64_t tile_lo = (wa + i) * kWTile;
-        const bool interior = tile_lo >= b0 && tile_lo + kWTile - 1 <= blast &&
-                              VEC && tile_lo + kWTile <= c.n;
+        const bool interior = tile_lo >= b0 && tile_lo + kWTile - 1 <= blast;
         if (interior) tile(std::false_type{}, i, fl);
         else tile(std::true_type{}, i, fl);
         __syncwarp();
-        if (i + 1 < cnt) stage(i + 1);
+        if (i + 1 < cnt) stage();
     }
 
     // ---- stitch: the area closed by each piece's first boundary
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             p -= 32;
         }
     }
-    if (lane == 0) c.aq[rank_first - 1] = kmin(acc, s_head[warp]);
+    if (lane == 0) c.aq[aq_slot<MARKED>(rank_first - 1)] = kmin(acc, s_head[warp]);
 }
 
 int contract_grid() {
@@ -537,8 +543,8 @@ int contract_grid() {
         int dev = 0, sms = 0, per_v = 0, per_s = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_v, k_contract<true>, NT, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, k_contract<false>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_v, k_contract<true, false>, NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, k_contract<false, true>, NT, 0);
         int per = per_v < per_s ? per_v : per_s;
         if (per < 1) per = 1;
         grid = sms * per;
@@ -567,7 +573,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out,
                     uint64_t* aq_len,
                     uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
-                    uint32_t epoch_off, cudaStream_t s) {
+                    uint32_t epoch_off, cudaStream_t s, bool marked) {
     if (n == 0) return 0;
     uint32_t G = 0, R = 0;
     contract_partition(n, &G, &R);
@@ -576,8 +582,11 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                       epoch_off};
     void* params[] = {&args};
     const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
-    cudaLaunchCooperativeKernel(vec ? reinterpret_cast<const void*>(k_contract<true>)
-                                    : reinterpret_cast<const void*>(k_contract<false>),
+    const void* fn = vec ? (marked ? reinterpret_cast<const void*>(k_contract<true, true>)
+                                   : reinterpret_cast<const void*>(k_contract<true, false>))
+                         : (marked ? reinterpret_cast<const void*>(k_contract<false, true>)
+                                   : reinterpret_cast<const void*>(k_contract<false, false>));
+    cudaLaunchCooperativeKernel(fn,
                                 dim3(G), dim3(NT), params, 0, s);
     return 1;  // launch errors surface through the caller's cudaGetLastError
 }

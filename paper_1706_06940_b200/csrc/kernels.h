@@ -81,7 +81,7 @@ size_t contract_status_words();    // status-arena words the contraction needs
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
-                    cudaStream_t s);
+                    cudaStream_t s, bool marked = false);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)
@@ -96,5 +96,14 @@ int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
                         const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cl,
                         uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s);
 int launch_keys_to_pos(uint64_t* t, uint64_t count, cudaStream_t s);
+// ST-RMQ_CON (SPEC.md "baseline"): marked entries + run fix-up, the two edge runs,
+// and the element-Sparse-Table query over E (2m+1 keys, m = *m_dev boundaries).
+int launch_marked_fill(const int32_t* A, const uint32_t* boundary, const uint64_t* m_dev,
+                       uint64_t m_max, uint64_t* E, cudaStream_t s);
+int launch_marked_edges(const int32_t* A, uint64_t n, const uint32_t* span, const uint64_t* m_dev,
+                        uint64_t* E, cudaStream_t s);
+int launch_query_st(const uint64_t* Q, const uint32_t* cleft, const uint32_t* cright_raw,
+                    uint64_t q, const uint64_t* ST, uint64_t stride, uint64_t* answers,
+                    cudaStream_t s);
 
 }  // namespace brmq

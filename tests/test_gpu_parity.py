@@ -14,7 +14,7 @@ from paper_1706_06940_b200 import (ENDPOINT_DTYPE, InvalidArgument, LogicError, 
 pytestmark = pytest.mark.gpu
 
 KS = [1, 2, 3, 7, 8, 64, 128, 256, 512, 1024, 2048, 4096]
-VARIANTS = ["bbst", "bbst_ml", "con_radix", "con_bitmap"]
+VARIANTS = ["bbst", "bbst_ml", "con_radix", "con_bitmap", "st_rmq_con"]
 
 
 def _values(r, n, kind):
@@ -67,6 +67,8 @@ def _solve(engine, variant, A, Q, k):
         if k == 0:
             return engine.solve_batch_bbst_ml(A, Q, (32, 0))
         return engine.solve_batch_bbst_ml(A, Q, (32, k if k % 32 == 0 and k > 32 else 512))
+    if variant == "st_rmq_con":  # the baseline has no block size
+        return engine.solve_batch_st_rmq_con(A, Q)
     kind = SortKind.Radix if variant == "con_radix" else SortKind.Bitmap
     return engine.solve_batch_bbst_con(A, Q, k, kind)
 
@@ -115,8 +117,9 @@ def test_edge_cases(engine, orc, variant):
     with pytest.raises(OutOfRange):
         _solve(engine, variant, A, make_queries([0], [100]), 512)
     # k = 0 -> invalid_argument (BbstConParams invariant k >= 1)
-    with pytest.raises(InvalidArgument):
-        _solve(engine, variant, A, make_queries([0], [5]), 0)
+    if variant != "st_rmq_con":  # no block size
+        with pytest.raises(InvalidArgument):
+            _solve(engine, variant, A, make_queries([0], [5]), 0)
     # the engine is still healthy after an error
     assert list(_solve(engine, variant, A, make_queries([3], [9]), 4)) == [9]
 
