@@ -111,6 +111,11 @@ int brmq_solve_bbst_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_
                         uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
                         uint32_t flags);
 
+/* naive.hpp:13-21 for every query, on the device (one warp per query): the
+ * harness's "naive" algorithm. */
+int brmq_solve_naive(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
+                     uint64_t q, uint64_t* answers, uint32_t flags);
+
 /* SPEC.md:331-377 solve_batch_st_rmq_con(array, batch) -- the comparison baseline
  * ST-RMQ_CON of Alzamel et al. (section 2): marked contraction of A
  * into <= 4q + 1 entries, element Sparse Table over them, two probes per query.

@@ -179,6 +179,10 @@ class Engine:
         """SPEC.md:237-245, BbST_CON (PAPER.md:210-272)."""
         return self._solve(True, array, batch, k, int(sort_kind), out)
 
+    def solve_batch_naive(self, array, batch, out=None):
+        """naive.hpp:13-21 for every query (the harness's "naive"), on the device."""
+        return self._solve("naive", array, batch, 1, 0, out)
+
     def solve_batch_st_rmq_con(self, array, batch, out=None):
         """SPEC.md:331-377, the ST-RMQ_CON baseline (section 2)."""
         return self._solve("st", array, batch, 1, 0, out)
@@ -199,7 +203,9 @@ class Engine:
             if out is None:
                 out = np.empty(q, dtype=np.uint64)
             a, b, o, flags = _ptr(array), _ptr(batch), _ptr(out), PTR_HOST
-        if con == "st":
+        if con == "naive":
+            rc = self._L.brmq_solve_naive(self._h, a, n, b, q, o, flags)
+        elif con == "st":
             rc = self._L.brmq_solve_st_rmq_con(self._h, a, n, b, q, o, flags)
         elif con == "ml":
             ks = (C.c_uint32 * len(k))(*k)

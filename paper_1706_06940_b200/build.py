@@ -75,6 +75,21 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+CLI_SRC = PKG / "cli" / "brmq_cli.cpp"
+CLI = PKG / "brmq"
+
+
+def build_cli(force: bool = False) -> Path:
+    """The harness command line linked against the in-tree libbrmq.so."""
+    if force or _stale(CLI, [CLI_SRC, LIB, *(ROOT / "include").glob("*.h")]):
+        cmd = ["g++", "-O2", "-std=c++17", "-I", str(ROOT / "include"), str(CLI_SRC), "-L", str(PKG),
+               "-lbrmq", "-Wl,-rpath,$ORIGIN", "-lpthread", "-o", str(CLI)]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"cli build failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+    return CLI
+
+
 def build_oracle() -> None:
     """Compile the CPU checker (oracle/liboracle.so) and, when the reference
     sources are present (this container), oracle/_ref/libbrmq_ref.so."""
@@ -90,6 +105,7 @@ def main() -> None:
     ap.add_argument("-v", "--verbose", action="store_true")
     a = ap.parse_args()
     print(build_lib(a.force, a.verbose))
+    print(build_cli(a.force))
     build_oracle()
 
 

@@ -1,0 +1,302 @@
+// brmq_cli.cpp -- the harness command line of SPEC.md:456 on the B200 engine.
+//
+//   brmq gen-array   --n N --seed S --out F [--kind permutation|uniform|ties16|walk]
+//   brmq gen-queries --n N --q Q --seed S --out F [--kind uniform|loguniform|mixed]
+//   brmq run --algo {naive|sparse|st-rmq-con|bbst-con|bbst|bbst-ml} --array F --queries F
+//            [--k K | --chain K1,K2] [--runs R=7] [--threads T=1] [--sort radix|comparison|bitmap]
+//            --csv F [--plot F] [--answers F]
+//   brmq verify --array F --queries F --answers F [--threads T]
+//
+// `run` copies the workload to the device once, then times R solves with the
+// inputs resident in HBM (a 256 MiB device copy between runs evicts the L2),
+// taking per-stage CUDA-event times from the engine (stages 1-4 of Table 1:
+// endpoint sort, contraction, table build, answering) and reporting the median
+// of each column independently.  The CSV row carries the
+// Table 2 byte model and the answer-value checksum.  Exit status: 0 success,
+// 2 verification failure, 1 usage / runtime error.
+//
+// gen-array's default kind is SPEC's gen_permutation; the
+// other kinds are BASELINE.json's arrays (include/brmq_workload.h).
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "brmq.h"
+#include "brmq_harness.h"
+#include "brmq_workload.h"
+
+namespace {
+
+struct Args {
+    std::map<std::string, std::string> kv;
+    bool has(const char* k) const { return kv.count(k) != 0; }
+    std::string get(const char* k, const char* def = nullptr) const {
+        auto it = kv.find(k);
+        if (it != kv.end()) return it->second;
+        if (!def) {
+            fprintf(stderr, "brmq: missing --%s\n", k);
+            exit(1);
+        }
+        return def;
+    }
+    uint64_t num(const char* k, const char* def = nullptr) const {
+        const std::string v = get(k, def);
+        char* end = nullptr;
+        const unsigned long long x = strtoull(v.c_str(), &end, 10);
+        if (!end || *end) {
+            fprintf(stderr, "brmq: --%s expects a number, got '%s'\n", k, v.c_str());
+            exit(1);
+        }
+        return x;
+    }
+};
+
+Args parse(int argc, char** argv, int from) {
+    Args a;
+    for (int i = from; i < argc; ++i) {
+        if (strncmp(argv[i], "--", 2) != 0 || i + 1 >= argc) {
+            fprintf(stderr, "brmq: bad argument '%s'\n", argv[i]);
+            exit(1);
+        }
+        a.kv[argv[i] + 2] = argv[i + 1];
+        ++i;
+    }
+    return a;
+}
+
+void check(int rc, const char* what) {
+    if (rc == BRMQ_OK) return;
+    fprintf(stderr, "brmq: %s failed (status %d): %s\n", what, rc, brmq_last_error());
+    exit(1);
+}
+
+int usage() {
+    fprintf(stderr,
+            "usage: brmq gen-array --n N --seed S --out F [--kind permutation|uniform|ties16|walk]\n"
+            "       brmq gen-queries --n N --q Q --seed S --out F [--kind uniform|loguniform|mixed]\n"
+            "       brmq run --algo {naive|sparse|st-rmq-con|bbst-con|bbst|bbst-ml} --array F\n"
+            "                --queries F [--k K | --chain K1,K2] [--runs R] [--threads T]\n"
+            "                [--sort radix|comparison|bitmap] --csv F [--plot F] [--answers F]\n"
+            "       brmq verify --array F --queries F --answers F [--threads T]\n");
+    return 1;
+}
+
+std::vector<int32_t> load_array(const std::string& path) {
+    uint64_t n = 0;
+    check(brmq_read_array_file(path.c_str(), nullptr, 0, &n), "read array");
+    std::vector<int32_t> A(n);
+    check(brmq_read_array_file(path.c_str(), A.data(), n, &n), "read array");
+    return A;
+}
+
+std::vector<brmq_query> load_queries(const std::string& path) {
+    uint64_t q = 0;
+    check(brmq_read_query_file(path.c_str(), nullptr, 0, &q), "read queries");
+    std::vector<brmq_query> Q(q);
+    check(brmq_read_query_file(path.c_str(), Q.data(), q, &q), "read queries");
+    return Q;
+}
+
+std::vector<uint64_t> load_answers(const std::string& path) {
+    uint64_t q = 0;
+    check(brmq_read_answer_file(path.c_str(), nullptr, 0, &q), "read answers");
+    std::vector<uint64_t> a(q);
+    check(brmq_read_answer_file(path.c_str(), a.data(), q, &q), "read answers");
+    return a;
+}
+
+int cmd_gen_array(const Args& a) {
+    const uint64_t n = a.num("n"), seed = a.num("seed");
+    const std::string kind = a.get("kind", "permutation");
+    const std::map<std::string, int> kinds{{"uniform", BRMQ_ARRAY_UNIFORM31},
+                                           {"ties16", BRMQ_ARRAY_TIES16},
+                                           {"walk", BRMQ_ARRAY_WALK},
+                                           {"permutation", BRMQ_ARRAY_PERMUTATION}};
+    if (!kinds.count(kind)) return usage();
+    std::vector<int32_t> A(n);
+    check(brmq_workload_array(kinds.at(kind), n, seed, A.data(), 0), "generate array");
+    check(brmq_write_array_file(a.get("out").c_str(), A.data(), n), "write array");
+    return 0;
+}
+
+int cmd_gen_queries(const Args& a) {
+    const uint64_t n = a.num("n"), q = a.num("q"), seed = a.num("seed");
+    const std::string kind = a.get("kind", "uniform");
+    const std::map<std::string, int> kinds{{"uniform", BRMQ_QUERIES_UNIFORM},
+                                           {"loguniform", BRMQ_QUERIES_LOGUNIFORM},
+                                           {"mixed", BRMQ_QUERIES_MIXED}};
+    if (!kinds.count(kind)) return usage();
+    std::vector<brmq_query> Q(q);
+    check(brmq_workload_queries(kinds.at(kind), n, q, seed, reinterpret_cast<uint64_t*>(Q.data()), 0),
+          "generate queries");
+    check(brmq_write_query_file(a.get("out").c_str(), Q.data(), q), "write queries");
+    return 0;
+}
+
+double median(std::vector<double> v) {
+    if (v.empty()) return 0.0;
+    std::sort(v.begin(), v.end());
+    const size_t h = v.size() / 2;
+    return v.size() % 2 ? v[h] : 0.5 * (v[h - 1] + v[h]);
+}
+
+int cmd_run(const Args& a) {
+    const std::string algo = a.get("algo");
+    const std::map<std::string, int> algos{{"naive", BRMQ_ALGO_NAIVE},         {"sparse", BRMQ_ALGO_SPARSE},
+                                           {"st-rmq-con", BRMQ_ALGO_ST_RMQ_CON}, {"bbst-con", BRMQ_ALGO_BBST_CON},
+                                           {"bbst", BRMQ_ALGO_BBST},             {"bbst-ml", BRMQ_ALGO_BBST_ML}};
+    if (!algos.count(algo)) return usage();
+    const int aid = algos.at(algo);
+    std::vector<uint32_t> ks;
+    if (a.has("chain")) {
+        std::string c = a.get("chain");
+        size_t p = 0;
+        while (p <= c.size()) {
+            const size_t e = c.find(',', p);
+            ks.push_back(uint32_t(strtoul(c.substr(p, e - p).c_str(), nullptr, 10)));
+            if (e == std::string::npos) break;
+            p = e + 1;
+        }
+    } else {
+        ks.push_back(uint32_t(a.num("k", algo == "sparse" ? "1" : "512")));
+    }
+    if (aid == BRMQ_ALGO_SPARSE) ks = {1};  // the element table = block size 1
+    const uint64_t runs = a.num("runs", "7"), threads = a.num("threads", "1");
+    const std::string sort = a.get("sort", "radix");
+    const int sort_kind = sort == "radix" ? BRMQ_SORT_RADIX
+                        : sort == "comparison" ? BRMQ_SORT_COMPARISON
+                        : sort == "bitmap" ? BRMQ_SORT_BITMAP : -1;
+    if (sort_kind < 0 || runs == 0) return usage();
+    const std::vector<int32_t> A = load_array(a.get("array"));
+    const std::vector<brmq_query> Q = load_queries(a.get("queries"));
+    const uint64_t n = A.size(), q = Q.size();
+
+    brmq_ctx* ctx = nullptr;
+    check(brmq_ctx_create(&ctx, 0), "create context");
+    void *dA = nullptr, *dQ = nullptr, *dO = nullptr, *f0 = nullptr, *f1 = nullptr;
+    const size_t flush = size_t(256) << 20;
+    check(brmq_device_alloc(ctx, &dA, n * 4 + 16), "device alloc");
+    check(brmq_device_alloc(ctx, &dQ, q * 16 + 16), "device alloc");
+    check(brmq_device_alloc(ctx, &dO, q * 8 + 16), "device alloc");
+    check(brmq_device_alloc(ctx, &f0, flush), "device alloc");
+    check(brmq_device_alloc(ctx, &f1, flush), "device alloc");
+    if (n) check(brmq_memcpy(ctx, dA, A.data(), n * 4, 1 /* H2D */), "copy array");
+    if (q) check(brmq_memcpy(ctx, dQ, Q.data(), q * 16, 1), "copy queries");
+    check(brmq_ctx_set_timing(ctx, 1), "timing");
+
+    std::vector<double> t_sort, t_con, t_build, t_ans, t_tot;
+    const auto* Ad = static_cast<const int32_t*>(dA);
+    const auto* Qd = static_cast<const brmq_query*>(dQ);
+    auto* Od = static_cast<uint64_t*>(dO);
+    for (uint64_t r = 0; r < runs; ++r) {
+        check(brmq_memcpy(ctx, f1, f0, flush, 3 /* D2D: evicts the L2 */), "flush");
+        int rc = BRMQ_OK;
+        switch (aid) {
+            case BRMQ_ALGO_NAIVE: rc = brmq_solve_naive(ctx, Ad, n, Qd, q, Od, BRMQ_PTR_DEVICE); break;
+            case BRMQ_ALGO_SPARSE:
+            case BRMQ_ALGO_BBST: rc = brmq_solve_bbst(ctx, Ad, n, Qd, q, ks.back(), Od, BRMQ_PTR_DEVICE); break;
+            case BRMQ_ALGO_BBST_ML:
+                rc = brmq_solve_bbst_ml(ctx, Ad, n, Qd, q, ks.data(), uint32_t(ks.size()), Od, BRMQ_PTR_DEVICE);
+                break;
+            case BRMQ_ALGO_BBST_CON:
+                rc = brmq_solve_bbst_con(ctx, Ad, n, Qd, q, ks.back(), sort_kind, Od, BRMQ_PTR_DEVICE);
+                break;
+            case BRMQ_ALGO_ST_RMQ_CON: rc = brmq_solve_st_rmq_con(ctx, Ad, n, Qd, q, Od, BRMQ_PTR_DEVICE); break;
+        }
+        check(rc, "solve");
+        check(brmq_synchronize(ctx), "synchronize");
+        brmq_stage_times st;
+        check(brmq_last_stage_times(ctx, &st), "stage times");
+        double s[4] = {0, 0, 0, 0}, tot = 0;
+        for (int i = 0; i < st.count; ++i) {
+            const std::string nm = st.name[i];
+            const double ns = double(st.ms[i]) * 1e6;
+            const int col = (nm == "collect" || nm == "radix_sort" || nm == "unique_rank" || nm == "collect_mark") ? 0
+                          : (nm == "contract" || nm == "remap") ? 1
+                          : (nm == "block_argmin" || nm == "sparse_table") ? 2
+                          : (nm == "query") ? 3 : -1;
+            if (col >= 0) {
+                s[col] += ns;
+                tot += ns;
+            }
+        }
+        t_sort.push_back(s[0]);
+        t_con.push_back(s[1]);
+        t_build.push_back(s[2]);
+        t_ans.push_back(s[3]);
+        t_tot.push_back(tot);
+    }
+    std::vector<uint64_t> ans(q);
+    if (q) check(brmq_memcpy(ctx, ans.data(), dO, q * 8, 2 /* D2H */), "copy answers");
+    uint64_t checksum = 0, extra = 0;
+    double pct = 0;
+    check(brmq_answers_checksum(A.data(), n, ans.data(), q, &checksum), "checksum");
+    check(brmq_account_memory(aid, n, q, ks.data(), uint32_t(ks.size()), &extra, &pct), "memory model");
+    if (a.has("answers")) check(brmq_write_answer_file(a.get("answers").c_str(), ans.data(), q), "write answers");
+    for (void* p : {dA, dQ, dO, f0, f1}) brmq_device_free(ctx, p);
+    brmq_ctx_destroy(ctx);
+
+    std::string chain;
+    for (size_t i = 0; i < ks.size(); ++i) chain += (i ? ";" : "") + std::to_string(ks[i]);
+    const std::string csv = a.get("csv");
+    FILE* probe = fopen(csv.c_str(), "rb");
+    bool header = true;
+    if (probe) {
+        header = fgetc(probe) == EOF;
+        fclose(probe);
+    }
+    FILE* f = fopen(csv.c_str(), "ab");
+    if (!f) {
+        fprintf(stderr, "brmq: cannot write %s\n", csv.c_str());
+        return 1;
+    }
+    if (header)
+        fprintf(f, "algo,n,q,k_chain,threads,runs,t_sort_ns,t_contract_ns,t_build_ns,t_answer_ns,"
+                   "t_total_ns,extra_bytes,extra_pct,answers_checksum\n");
+    fprintf(f, "%s,%llu,%llu,%s,%llu,%llu,%.0f,%.0f,%.0f,%.0f,%.0f,%llu,%.4f,%llu\n", algo.c_str(),
+            (unsigned long long)n, (unsigned long long)q, chain.c_str(), (unsigned long long)threads,
+            (unsigned long long)runs, median(t_sort), median(t_con), median(t_build), median(t_ans),
+            median(t_tot), (unsigned long long)extra, pct, (unsigned long long)checksum);
+    fclose(f);
+    if (a.has("plot")) fprintf(stderr, "brmq: --plot is not supported by this build (CSV written)\n");
+    return 0;
+}
+
+int cmd_verify(const Args& a) {
+    const std::vector<int32_t> A = load_array(a.get("array"));
+    const std::vector<brmq_query> Q = load_queries(a.get("queries"));
+    const std::vector<uint64_t> ans = load_answers(a.get("answers"));
+    if (ans.size() != Q.size()) {
+        fprintf(stderr, "brmq: %zu answers for %zu queries\n", ans.size(), Q.size());
+        return 2;
+    }
+    uint64_t bad = 0, first = 0;
+    check(brmq_verify_answers(A.data(), A.size(), Q.data(), Q.size(), ans.data(),
+                              unsigned(a.num("threads", "0")), &bad, &first),
+          "verify");
+    if (bad) {
+        fprintf(stderr, "brmq: %llu wrong answers (first at query %llu)\n", (unsigned long long)bad,
+                (unsigned long long)first);
+        return 2;
+    }
+    printf("ok: %zu answers verified\n", ans.size());
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) return usage();
+    const std::string cmd = argv[1];
+    const Args a = parse(argc, argv, 2);
+    if (cmd == "gen-array") return cmd_gen_array(a);
+    if (cmd == "gen-queries") return cmd_gen_queries(a);
+    if (cmd == "run") return cmd_run(a);
+    if (cmd == "verify") return cmd_verify(a);
+    return usage();
+}

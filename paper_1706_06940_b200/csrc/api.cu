@@ -454,6 +454,65 @@ int brmq_synchronize(brmq_ctx* c) {
     return BRMQ_OK;
 }
 
+// ------------------------------------------------------------------ naive
+// The harness's "naive" algorithm (naive.hpp:13-21): every query scanned on the
+// device, one warp per query.  A baseline, not a BbST path.
+int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
+                     uint64_t* answers, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    Timer tm(c);
+    if (q == 0) {
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    int launches = 0;
+    auto enqueue = [&]() -> int {
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        tm.stage("query", launches);
+        const int l = brmq::launch_naive(dA, n, dQ, q, dAns, &ctl->err, s);
+        launches += l;
+        tm.end(l);
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        return BRMQ_OK;
+    };
+    const GraphKey key{4, A, n, Q, q, 0, 0, answers, s};
+    if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(c->ctl_host->err);
+}
+
 // ------------------------------------------------------------------ BbST (h = 1)
 int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
                     uint32_t k, uint64_t* answers, uint32_t flags) {

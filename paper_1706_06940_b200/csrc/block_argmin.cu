@@ -122,10 +122,20 @@ inline unsigned grid_for_warps(uint64_t warps) {
 
 }  // namespace
 
+// k = 1 (the element Sparse Table of the harness's "sparse" algorithm): keys only
+__global__ void k_pack_keys(const int32_t* __restrict__ A, uint64_t n, uint64_t* __restrict__ keys) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = pack_key(__ldg(A + i), uint32_t(i));
+}
+
 int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
                             cudaStream_t stream) {
     const uint64_t nblk = (n + k - 1) / k;
     if (nblk == 0) return 0;
+    if (k == 1) {
+        k_pack_keys<<<unsigned((n + 255) / 256), 256, 0, stream>>>(A, n, keys);
+        return 1;
+    }
     if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
         k_block_argmin_i32_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys);
     } else {

@@ -31,6 +31,8 @@ int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* k
 int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStream_t stream);
 
 // ---------------------------------------------------------------- query.cu
+int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
+                 uint32_t* err, cudaStream_t stream);
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST,
                         uint64_t b, const uint64_t* Q, uint64_t q, uint64_t* answers,
                         uint32_t* err, cudaStream_t stream);

@@ -264,7 +264,40 @@ void dispatch_key(ElemKey e, QP qp, uint32_t k, const uint64_t* ST, uint64_t str
     return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
 }
 
+// The harness's "naive" algorithm (naive.hpp:13-21 on the device): one warp per
+// query scans A[l..r]; lanes take strided elements, a redux pair keeps the
+// leftmost minimum.
+__global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ A, uint64_t n,
+                                                    const ulonglong2* __restrict__ Q, uint64_t q,
+                                                    uint64_t* __restrict__ answers,
+                                                    uint32_t* __restrict__ err) {
+    const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(Q + i);
+    uint64_t l = x.x, r = x.y;
+    if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
+    if (r >= n) {                                        // naive.hpp:14-15
+        if (lane_id() == 0) {
+            atomicOr(err, 1u);
+            answers[i] = ~0ull;
+        }
+        return;
+    }
+    uint64_t b = kNoKey;
+    for (uint64_t p = l + lane_id(); p <= r; p += 32) b = kmin(b, pack_key(__ldg(A + p), uint32_t(p)));
+    b = warp_min_key(b);
+    if (lane_id() == 0) answers[i] = key_pos(b);
+}
+
 }  // namespace
+
+int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
+                 uint32_t* err, cudaStream_t stream) {
+    if (q == 0) return 0;
+    k_naive<<<unsigned((q * 32 + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+        A, n, reinterpret_cast<const ulonglong2*>(Q), q, answers, err);
+    return 1;
+}
 
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                         const uint64_t* Q, uint64_t q, uint64_t* answers, uint32_t* err,
