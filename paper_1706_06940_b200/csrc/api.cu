@@ -751,13 +751,12 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
             tm.end(0);
         }
-        k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, n_epochs);  // epochs of this solve
-        launches += 1;
+        // the epochs of this solve are reserved by the first kernel (k_collect)
         // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
             l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->rcnt, R,
-                                     ctl->span, &ctl->err, s);
+                                     ctl->span, &ctl->err, s, c->epoch_dev, n_epochs);
             launches += l;
             tm.end(l);
         } else {
@@ -766,7 +765,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
             auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
             tm.stage("collect", launches);
-            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s);
+            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s,
+                                     c->epoch_dev, n_epochs);
             launches += l;
             tm.end(l);
             tm.stage("radix_sort", launches);
@@ -902,14 +902,14 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
             CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
             tm.end(0);
         }
-        k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, n_epochs);
-        launches += 1;
+        // the epochs of this solve are reserved by the first kernel (k_collect)
         auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
         auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
         auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
         auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
         tm.stage("collect", launches);
-        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s);
+        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s,
+                                 c->epoch_dev, n_epochs);
         launches += l;
         tm.end(l);
         tm.stage("radix_sort", launches);

@@ -43,7 +43,11 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                                                       uint32_t* __restrict__ bitmap,
                                                       uint32_t* __restrict__ rcnt, uint32_t R,
                                                       uint32_t G, uint32_t* __restrict__ span,
-                                                      uint32_t* __restrict__ err) {
+                                                      uint32_t* __restrict__ err,
+                                                      uint32_t* __restrict__ epoch_bump,
+                                                      uint32_t epoch_by) {
+    // the solve's epoch reservation rides on this first kernel (no extra launch)
+    if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) *epoch_bump += epoch_by;
     __shared__ uint32_t s_lo, s_hi;
     __shared__ uint32_t s_hist[kMaxContractRanges];
     if (threadIdx.x == 0) { s_lo = 0xFFFFFFFFu; s_hi = 0; }
@@ -363,14 +367,15 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 // ------------------------------------------------------------------ launchers
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
-                   uint32_t* err, cudaStream_t s) {
+                   uint32_t* err, cudaStream_t s, uint32_t* epoch_bump, uint32_t epoch_by) {
     if (q == 0) return 0;
-    const unsigned grid = g256(q) < 148u * 16u ? g256(q) : 148u * 16u;
+    const unsigned cap = 148u * 16u;
+    const unsigned grid = g256(q) < cap ? g256(q) : cap;
     uint32_t G = 0, R = 1;
     if (bitmap) contract_partition(n, &G, &R);
     if (bitmap && R != range_tiles) return -1;  // caller and kernel disagree on the partition
     k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
-                                           bitmap, rcnt, R, G, span, err);
+                                           bitmap, rcnt, R, G, span, err, epoch_bump, epoch_by);
     return 1;
 }
 

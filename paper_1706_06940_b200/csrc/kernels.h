@@ -68,7 +68,8 @@ constexpr int kContractTileLog2 = 12;  // 4096-position tiles
 void contract_partition(uint64_t n, uint32_t* G, uint32_t* R);
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
-                   uint32_t* err, cudaStream_t s);
+                   uint32_t* err, cudaStream_t s,
+                   uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
 size_t unique_status_words(uint64_t m);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
