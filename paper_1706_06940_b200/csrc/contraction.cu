@@ -127,15 +127,18 @@ __device__ __forceinline__ uint64_t row_min(const RW& rw, uint32_t r, int lo, in
     return pack_key(bv, uint32_t(rw.pos(r, bi)));
 }
 
-// Per-thread closing of the areas whose right boundary (bit of fl) lies in
-// [lo, hi] of row r; `cur` = open-segment key entering lo, `rank` =
-// boundaries before.  Used when boundaries are dense.
+// Dense rows, one pass: the areas between consecutive boundaries of row r in
+// [lo, hi] are stored (the first boundary has global rank `rank`, so the second
+// closes area `rank`, ...); hp = min over [lo, first boundary] (the part of the
+// area the row's first boundary closes, completed after the warp scan), run =
+// min over [last boundary, hi] (the open segment the row hands on).
 template <bool MARKED, class RW>
-__device__ __forceinline__ void row_close_areas(const RW& rw, uint32_t r, uint32_t fl, int lo,
-                                                int hi, uint64_t cur, uint64_t rank,
-                                                uint64_t* __restrict__ aq) {
+__device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, int lo, int hi,
+                                         uint64_t rank, uint64_t* __restrict__ aq, uint64_t& hp,
+                                         uint64_t& run) {
     int32_t rv = 0x7FFFFFFF;
     int ri = -1;
+    bool seen = false;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
         if (4 * c + 3 < lo || 4 * c > hi) continue;
@@ -146,12 +149,15 @@ __device__ __forceinline__ void row_close_areas(const RW& rw, uint32_t r, uint32
             if (j < lo || j > hi) continue;
             const int32_t v = comp(x, e);
             if ((fl >> j) & 1u) {
-                uint64_t k = cur;
+                uint64_t k = pack_key(v, uint32_t(rw.pos(r, j)));  // inclusive right end
                 if (ri >= 0) k = kmin(k, pack_key(rv, uint32_t(rw.pos(r, ri))));
-                k = kmin(k, pack_key(v, uint32_t(rw.pos(r, j))));  // inclusive right end
-                if (rank > 0) aq[aq_slot<MARKED>(rank - 1)] = k;
-                ++rank;
-                cur = kNoKey;
+                if (seen) {
+                    aq[aq_slot<MARKED>(rank)] = k;
+                    ++rank;
+                } else {
+                    hp = k;
+                    seen = true;
+                }
                 rv = v;  // the boundary element opens the next area
                 ri = j;
             } else if (v < rv || ri < 0) {
@@ -160,6 +166,7 @@ __device__ __forceinline__ void row_close_areas(const RW& rw, uint32_t r, uint32
             }
         }
     }
+    run = ri >= 0 ? pack_key(rv, uint32_t(rw.pos(r, ri))) : kNoKey;
 }
 
 struct ContractArgs {
@@ -346,12 +353,11 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         }
         const bool dense = __popc(fm) > kDense;
 
-        // pass 1: open-segment key at the right end of the lane's row
+        // pass 1: open-segment key at the right end of the lane's row; a dense
+        // tile's flagged rows are handled in one pass below instead
         uint64_t run = kNoKey;
-        if (any && (fl == 0 || dense)) {
-            const int lo = fl ? 31 - __clz(fl) : jlo;
-            run = (!GEN && fl == 0) ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, lo, jhi);
-        }
+        if (any && fl == 0)
+            run = !GEN ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, jlo, jhi);
         uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (!dense) {  // sparse flagged rows: one element per lane
             for (unsigned m = fm; m; m &= m - 1) {
@@ -377,38 +383,41 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         SegMin wt;             // warp-tile total
         uint32_t wc;
         if (dense) {
-            SegMin inc{run, cntb != 0};
+            // ranks first (a count scan), then one pass per flagged row: its inner
+            // areas are stored at once, its head / tail parts join the warp scan
             uint32_t cinc = cntb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t cy = __shfl_up_sync(kFull, cinc, o);
+                if (lane >= uint32_t(o)) cinc += cy;
+            }
+            wc = __shfl_sync(kFull, cinc, 31);
+            const uint64_t rank = rank_run + (cinc - cntb);
+            uint64_t hp = kNoKey;
+            if (any && fl) row_pass<MARKED>(rs, lane, fl, jlo, jhi, rank, c.aq, hp, run);
+            SegMin inc{run, cntb != 0};
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 SegMin y;
                 y.k = __shfl_up_sync(kFull, inc.k, o);
                 y.f = __shfl_up_sync(kFull, inc.f, o);
-                const uint32_t cy = __shfl_up_sync(kFull, cinc, o);
-                if (lane >= uint32_t(o)) {
-                    inc = seg_combine(y, inc);
-                    cinc += cy;
-                }
+                if (lane >= uint32_t(o)) inc = seg_combine(y, inc);
             }
             wt.k = __shfl_sync(kFull, inc.k, 31);
             wt.f = __shfl_sync(kFull, inc.f, 31);
-            wc = __shfl_sync(kFull, cinc, 31);
             SegMin we;
             we.k = __shfl_up_sync(kFull, inc.k, 1);
             we.f = __shfl_up_sync(kFull, inc.f, 1);
-            uint32_t wce = __shfl_up_sync(kFull, cinc, 1);
-            if (lane == 0) { we = SegMin{kNoKey, 0}; wce = 0; }
+            if (lane == 0) we = SegMin{kNoKey, 0};
             if (fl) {
-                const SegMin in = seg_combine(carry, we);
-                const uint64_t rank = rank_run + wce;
+                const SegMin in = seg_combine(carry, we);  // open segment entering the row
                 my_rank = rank;
+                const uint64_t first = kmin(in.k, hp);   // the area the row's first boundary closes
                 if (in.f) {
-                    row_close_areas<MARKED>(rs, lane, fl, jlo, jhi, in.k, rank, c.aq);
+                    c.aq[aq_slot<MARKED>(rank - 1)] = first;
                 } else {  // first boundary of the piece: its area opened in an earlier piece
-                    const int f = __ffs(fl) - 1;
-                    head = kmin(in.k, row_min<false>(rs, lane, jlo, f));
+                    head = first;
                     head_set = true;
-                    row_close_areas<MARKED>(rs, lane, fl & (fl - 1), f, jhi, kNoKey, rank + 1, c.aq);
                 }
             }
         } else {
