@@ -755,8 +755,9 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
-            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, ctl->rcnt, R,
+            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, nullptr, R,
                                      ctl->span, &ctl->err, s, c->epoch_dev, n_epochs);
+            l += brmq::launch_range_count(c->bitmap, ctl->span, n, ctl->rcnt, s);
             launches += l;
             tm.end(l);
         } else {

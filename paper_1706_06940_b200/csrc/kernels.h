@@ -70,6 +70,9 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
                    uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
                    uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
+// rcnt[g] = boundaries of contraction range g, popcounted from the bitmap
+int launch_range_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* rcnt,
+                       cudaStream_t s);
 size_t unique_status_words(uint64_t m);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
