@@ -790,12 +790,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
                                   c->epoch_dev, 0, s);
         launches += l;
         tm.end(l);
-        if (use_bitmap) {
-            tm.stage("remap", launches);
-            l = brmq::launch_remap_bitmap(dQ, q, n, reinterpret_cast<uint2*>(P(i_wi)), cl, cr, s);
-            launches += l;
-            tm.end(l);
-        }
+        // (bitmap pipeline: the query remap is folded into the query kernel)
         tm.stage("block_argmin", launches);
         l = brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
         launches += l;
@@ -805,7 +800,11 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr, q, dAns, s);
+        l = use_bitmap ? brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ,
+                                                          reinterpret_cast<uint2*>(P(i_wi)), n, q,
+                                                          dAns, s)
+                       : brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr,
+                                                       q, dAns, s);
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;

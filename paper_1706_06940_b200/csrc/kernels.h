@@ -41,6 +41,10 @@ int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t
 int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                     const uint64_t* sub, const uint64_t* Q, uint64_t q, uint64_t* answers,
                     uint32_t* err, cudaStream_t stream);
+// bitmap pipeline: contracted coordinates from the contraction's word_info
+int launch_query_contracted_wi(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
+                               const uint64_t* Q, const uint2* word_info, uint64_t n, uint64_t q,
+                               uint64_t* answers, cudaStream_t stream);
 int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint32_t k,
                             const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
                             const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,

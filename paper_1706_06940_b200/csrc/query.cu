@@ -125,6 +125,26 @@ struct QueryContracted {
     }
 };
 
+// Bitmap pipeline: the contracted coordinates come straight from the per-word
+// (rank prefix, bits) the contraction emitted -- remap_queries_from_sorted
+// (contraction.cpp:174-199) folded into the query kernel.
+struct QueryContractedWI {
+    const uint64_t* Q;
+    const uint2* word_info;
+    uint64_t n;
+    __device__ __forceinline__ Resolved resolve(uint64_t i) const {
+        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        uint64_t l = x.x, r = x.y;
+        if (l > r) { const uint64_t t = l; l = r; r = t; }
+        if (r >= n) { r = n - 1; if (l > r) l = r; }  // already reported by the endpoint stage
+        const uint2 wl = __ldg(word_info + (l >> 5)), wr = __ldg(word_info + (r >> 5));
+        const uint32_t cl = wl.x + __popc(wl.y & ((1u << (l & 31)) - 1u));
+        const uint32_t cr = wr.x + __popc(wr.y & ((1u << (r & 31)) - 1u));
+        Resolved o{cl, uint64_t(cr) - 1, l, r, l, cl == cr};
+        return o;
+    }
+};
+
 template <class E>
 __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64_t hi) {
     uint64_t b = kNoKey;
@@ -304,6 +324,14 @@ int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t
                         cudaStream_t stream) {
     if (q == 0) return 0;
     dispatch_i32(ElemI32{A, n}, QueryDirect{Q, n, err}, k, ST, b, q, answers, stream);
+    return 1;
+}
+
+int launch_query_contracted_wi(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
+                               const uint64_t* Q, const uint2* word_info, uint64_t n, uint64_t q,
+                               uint64_t* answers, cudaStream_t stream) {
+    if (q == 0) return 0;
+    dispatch_key(ElemKey{AQ}, QueryContractedWI{Q, word_info, n}, k, ST, b_max, q, answers, stream);
     return 1;
 }
 
