@@ -710,6 +710,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const size_t i_st = cv.add(size_t(L) * b_max * 8);
     Carve sv;  // status arena
     const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
+    const size_t i_pc = cv.add(size_t(brmq::kMaxContractRanges) * brmq::kContractWarps * 4);
     size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_rst = 0, i_ust = 0, i_wi = 0;
     if (use_bitmap) {
         i_wi = cv.add((n / 32 + 2) * 8);
@@ -735,6 +736,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
     auto* cst = S(i_cst);
+    auto* pcnt = reinterpret_cast<uint32_t*>(P(i_pc));
     const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
@@ -757,7 +759,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             tm.stage("collect_mark", launches);
             l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, nullptr, R,
                                      ctl->span, &ctl->err, s, c->epoch_dev, n_epochs);
-            l += brmq::launch_range_count(c->bitmap, ctl->span, n, ctl->rcnt, s);
+            l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
             launches += l;
             tm.end(l);
         } else {
@@ -787,7 +789,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, !use_bitmap, AQ,
                                   &ctl->nb, &ctl->aq_len,
                                   use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
-                                  c->epoch_dev, 0, s);
+                                  c->epoch_dev, 0, s, false, use_bitmap ? pcnt : nullptr);
         launches += l;
         tm.end(l);
         // (bitmap pipeline: the query remap is folded into the query kernel)

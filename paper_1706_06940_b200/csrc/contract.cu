@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                     atomicAdd(s_hist + (lo >> kContractTileLog2) / R, 1u);
                 if (!(atomicOr(bitmap + (hi >> 5), bh) & bh))
                     atomicAdd(s_hist + (hi >> kContractTileLog2) / R, 1u);
-            } else {  // marks only (fire-and-forget reductions); counted by k_range_count
+            } else {  // marks only (fire-and-forget reductions); counted by k_piece_count (contraction.cu)
                 atomicOr(bitmap + (lo >> 5), bl);
                 atomicOr(bitmap + (hi >> 5), bh);
             }
@@ -103,35 +103,6 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
             atomicMax(span + 0, ~s_lo);
             atomicMax(span + 1, s_hi);
         }
-    }
-}
-
-// Boundaries per contraction range (rcnt[g]) from the finished bitmap: one CTA
-// per range popcounts its words (ranges of R tiles of 128 words).
-__global__ void __launch_bounds__(kThreads) k_range_count(const uint4* __restrict__ bitmap4,
-                                                          const uint32_t* __restrict__ span,
-                                                          uint32_t R, uint32_t* __restrict__ rcnt) {
-    __shared__ uint32_t s_w[kThreads / 32];
-    const uint32_t b0 = ~span[0], blast = span[1];
-    if (b0 > blast) return;
-    const uint64_t g = blockIdx.x;
-    const uint64_t t0 = g * R, t1 = t0 + R;  // tiles [t0, t1)
-    if (t0 > (blast >> kContractTileLog2) || t1 <= (b0 >> kContractTileLog2)) {
-        if (threadIdx.x == 0) rcnt[g] = 0;
-        return;
-    }
-    uint32_t c = 0;
-    for (uint64_t v = t0 * 32 + threadIdx.x; v < t1 * 32; v += kThreads) {  // 32 uint4 per tile
-        const uint4 w = __ldg(bitmap4 + v);
-        c += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
-    }
-    c = __reduce_add_sync(kFull, c);
-    if (lane_id() == 0) s_w[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        c = threadIdx.x < kThreads / 32 ? s_w[threadIdx.x] : 0u;
-        c = __reduce_add_sync(kFull, c);
-        if (threadIdx.x == 0) rcnt[g] = c;
     }
 }
 
@@ -414,14 +385,6 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
 }
 
 size_t unique_status_words(uint64_t m) { return (m + kTile - 1) / kTile; }
-
-int launch_range_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* rcnt,
-                       cudaStream_t s) {
-    uint32_t G = 0, R = 0;
-    contract_partition(n, &G, &R);
-    k_range_count<<<G, kThreads, 0, s>>>(reinterpret_cast<const uint4*>(bitmap), span, R, rcnt);
-    return 1;
-}
 
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n, uint32_t* boundary,
                   uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* rfirst,

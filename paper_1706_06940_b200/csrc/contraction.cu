@@ -50,6 +50,7 @@ namespace brmq {
 namespace {
 
 constexpr int NW = 8;               // warps per CTA, one stream each (2 CTAs per SM at 128 registers)
+static_assert(NW == int(kContractWarps), "piece layout shared with the endpoint stage");
 constexpr int NT = NW * 32;
 constexpr int kRow = 32;            // positions per lane = one 128-byte row
 constexpr int kWTile = 32 * kRow;   // 1024 positions = 4 KB per warp tile
@@ -169,6 +170,58 @@ __device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, 
     run = ri >= 0 ? pack_key(rv, uint32_t(rw.pos(r, ri))) : kNoKey;
 }
 
+// Warp `warp`'s piece of CTA `cta`'s range: warp tiles [wa, wa + cnt) of range
+// cta (R tiles), clipped to the span [b0, blast]; cnt = 0 when empty.  Shared by
+// the contraction and the piece-count kernel, so both cut identically.
+struct Piece {
+    uint64_t wa, cnt;
+};
+__device__ __forceinline__ Piece piece_of(uint64_t cta, uint32_t warp, uint64_t R, uint32_t b0,
+                                          uint32_t blast) {
+    const uint64_t tfirst = b0 / kTile, tlast = blast / kTile, ra = cta * R;
+    const uint64_t ta = ra > tfirst ? ra : tfirst;
+    const uint64_t tb = ra + R - 1 < tlast ? ra + R - 1 : tlast;
+    if (ta > tb) return Piece{0, 0};
+    const uint64_t w0 = ta * 4 > b0 / kWTile ? ta * 4 : b0 / kWTile;
+    const uint64_t w1 = tb * 4 + 3 < blast / kWTile ? tb * 4 + 3 : blast / kWTile;
+    const uint64_t per = (w1 - w0 + NW) / NW;
+    const uint64_t wa = w0 + warp * per;
+    const uint64_t wb = wa + per - 1 < w1 ? wa + per - 1 : w1;
+    return Piece{wa, wa <= wb ? wb - wa + 1 : 0};
+}
+
+// Boundaries per piece (pcnt[g * NW + w]) and per range (rcnt[g]), popcounted
+// from the finished bitmap (L2-resident): one CTA per range, one warp per piece.
+__global__ void __launch_bounds__(NT) k_piece_count(const uint32_t* __restrict__ bitmap,
+                                                    const uint32_t* __restrict__ span, uint64_t R,
+                                                    uint32_t* __restrict__ pcnt,
+                                                    uint32_t* __restrict__ rcnt) {
+    __shared__ uint32_t s_c[NW];
+    const uint32_t b0 = ~span[0], blast = span[1];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t k = 0;
+    if (b0 <= blast) {
+        const Piece pc = piece_of(blockIdx.x, warp, R, b0, blast);
+        const uint4* w4 = reinterpret_cast<const uint4*>(bitmap + pc.wa * 32);
+        for (uint64_t j = lane; j < pc.cnt * 8; j += 32) {
+            const uint4 w = __ldg(w4 + j);
+            k += __popc(w.x) + __popc(w.y) + __popc(w.z) + __popc(w.w);
+        }
+    }
+    k = __reduce_add_sync(kFull, k);
+    if (lane == 0) {
+        pcnt[uint64_t(blockIdx.x) * NW + warp] = k;
+        s_c[warp] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t += s_c[w];
+        rcnt[blockIdx.x] = t;
+    }
+}
+
 struct ContractArgs {
     const int32_t* A;
     uint64_t n;
@@ -183,6 +236,7 @@ struct ContractArgs {
     uint32_t prefix;
     uint64_t* st_part;   // [G] epoch-tagged partial descriptors
     uint64_t* key_tail;  // [G]
+    const uint32_t* pcnt;  // nullable: [G * NW] boundaries per piece (k_piece_count)
     const uint32_t* epoch_dev;  // device epoch counter (bumped once per solve)
     uint32_t epoch_off;
 };
@@ -213,13 +267,9 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
     const uint64_t cfirst = tfirst / R;  // the CTA holding b0
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
 
-    // this warp's piece: warp tiles [wa, wb] of the range, clipped to the span
-    const uint64_t w0 = ta * 4 > b0 / kWTile ? ta * 4 : b0 / kWTile;
-    const uint64_t w1 = tb * 4 + 3 < blast / kWTile ? tb * 4 + 3 : blast / kWTile;
-    const uint64_t per = (w1 - w0 + NW) / NW;
-    const uint64_t wa = w0 + warp * per;
-    const uint64_t wb = wa + per - 1 < w1 ? wa + per - 1 : w1;
-    const uint64_t cnt = wa <= wb ? wb - wa + 1 : 0;
+    // this warp's piece: warp tiles [wa, wa + cnt) of the range, clipped to the span
+    const Piece pc = piece_of(cta, warp, R, b0, blast);
+    const uint64_t wa = pc.wa, cnt = pc.cnt;
 
     // Warp tile i (1024 positions): 8 coalesced 16-byte loads per lane into
     // registers one tile ahead, stored transposed into the warp's rows so that
@@ -266,8 +316,8 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
     // warp's from a popcount of its piece of the bitmap (loads overlap the ring)
     {
         const uint4* w4 = reinterpret_cast<const uint4*>(c.bitmap + wa * 32);
-        const uint64_t nvec = cnt * 8;
-        uint32_t k = 0;
+        const uint64_t nvec = c.pcnt ? 0 : cnt * 8;  // counted already by k_piece_count
+        uint32_t k = c.pcnt ? __ldg(c.pcnt + cta * NW + warp) : 0u;
         for (uint64_t j0 = lane; j0 < nvec; j0 += 32 * 8) {
             uint4 w[8];
 #pragma unroll
@@ -276,7 +326,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
 #pragma unroll
             for (int u = 0; u < 8; ++u) k += __popc(w[u].x) + __popc(w[u].y) + __popc(w[u].z) + __popc(w[u].w);
         }
-        k = __reduce_add_sync(kFull, k);
+        if (!c.pcnt) k = __reduce_add_sync(kFull, k);
         uint32_t pre = 0;  // boundaries of earlier ranges (sum form)
         if (!c.prefix)
             for (uint64_t j = tid; j < cta; j += NT) pre += __ldg(c.rcnt + j);
@@ -568,6 +618,14 @@ size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
 size_t contract_bitmap_words(uint64_t n) { return contract_tiles(n) * (kTile / 32) + 4; }
 size_t contract_status_words() { return size_t(2) * kMaxContractRanges; }  // st_part, key_tail
 
+int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* pcnt,
+                       uint32_t* rcnt, cudaStream_t s) {
+    uint32_t G = 0, R = 0;
+    contract_partition(n, &G, &R);
+    k_piece_count<<<G, NT, 0, s>>>(bitmap, span, R, pcnt, rcnt);
+    return 1;
+}
+
 void contract_partition(uint64_t n, uint32_t* G, uint32_t* R) {
     const uint64_t tiles = contract_tiles(n);
     uint64_t g = uint64_t(contract_grid());
@@ -582,12 +640,12 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out,
                     uint64_t* aq_len,
                     uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
-                    uint32_t epoch_off, cudaStream_t s, bool marked) {
+                    uint32_t epoch_off, cudaStream_t s, bool marked, const uint32_t* pcnt) {
     if (n == 0) return 0;
     uint32_t G = 0, R = 0;
     contract_partition(n, &G, &R);
     ContractArgs args{A, n, bitmap, span, aq, nb_out, aq_len, word_info, rcnt, R,
-                      prefix ? 1u : 0u, status, status + kMaxContractRanges, epoch_dev,
+                      prefix ? 1u : 0u, status, status + kMaxContractRanges, pcnt, epoch_dev,
                       epoch_off};
     void* params[] = {&args};
     const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;

@@ -74,9 +74,11 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
                    uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
                    uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
-// rcnt[g] = boundaries of contraction range g, popcounted from the bitmap
-int launch_range_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* rcnt,
-                       cudaStream_t s);
+// Boundaries per contraction piece (pcnt[g * 8 + w], 8 warps per range) and per
+// range (rcnt[g]), popcounted from the bitmap.
+constexpr uint32_t kContractWarps = 8;
+int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* pcnt,
+                       uint32_t* rcnt, cudaStream_t s);
 size_t unique_status_words(uint64_t m);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
@@ -91,7 +93,8 @@ size_t contract_status_words();    // status-arena words the contraction needs
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
-                    cudaStream_t s, bool marked = false);
+                    cudaStream_t s, bool marked = false,
+                    const uint32_t* pcnt = nullptr);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)
