@@ -111,6 +111,17 @@ int brmq_solve_bbst_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_
                         uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
                         uint32_t flags);
 
+/* Sharded BbST: this device holds A[offset, offset + n_shard) of an
+ * array of n_total.  keys[i] = packed key (((uint32)v ^ 0x80000000) << 32 | pos)
+ * of the leftmost minimum of query i restricted to the shard, with pos GLOBAL,
+ * or UINT64_MAX when the query misses the shard.  The answer of query i over
+ * the whole array is (uint32)(min over shards of keys[i]) -- one min-allreduce
+ * of q uint64 (NCCL over NVLink) combines the devices exactly.  Query bounds
+ * are checked against n_total (BRMQ_ERANGE). */
+int brmq_solve_bbst_shard(brmq_ctx* ctx, const int32_t* A, uint64_t n_shard, uint64_t offset,
+                          uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
+                          uint64_t* keys, uint32_t flags);
+
 /* naive.hpp:13-21 for every query, on the device (one warp per query): the
  * harness's "naive" algorithm. */
 int brmq_solve_naive(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,

@@ -179,6 +179,28 @@ class Engine:
         """SPEC.md:237-245, BbST_CON (PAPER.md:210-272)."""
         return self._solve(True, array, batch, k, int(sort_kind), out)
 
+    def solve_batch_bbst_shard(self, shard, batch, offset: int, n_total: int, k: int = 512,
+                               out=None):
+        """Packed keys of every query restricted to A[offset, offset + len(shard)) with
+        global positions (UINT64_MAX when the query misses the shard); the min over
+        shards is the answer's key (include/brmq.h brmq_solve_bbst_shard)."""
+        if _is_cuda_tensor(shard):
+            import torch
+            ns, q = shard.numel(), batch.numel() // 2
+            if out is None:
+                out = torch.empty(q, dtype=torch.int64, device=shard.device)
+            a, b, o, flags = shard.data_ptr(), batch.data_ptr(), out.data_ptr(), PTR_DEVICE
+        else:
+            shard = np.ascontiguousarray(shard, dtype=np.int32)
+            batch = _as_queries(batch)
+            ns, q = shard.shape[0], batch.shape[0]
+            if out is None:
+                out = np.empty(q, dtype=np.uint64)
+            a, b, o, flags = _ptr(shard), _ptr(batch), _ptr(out), PTR_HOST
+        _check(self._L.brmq_solve_bbst_shard(self._h, a, ns, int(offset), int(n_total), b, q,
+                                             int(k), o, flags))
+        return out
+
     def solve_batch_naive(self, array, batch, out=None):
         """naive.hpp:13-21 for every query (the harness's "naive"), on the device."""
         return self._solve("naive", array, batch, 1, 0, out)

@@ -454,6 +454,88 @@ int brmq_synchronize(brmq_ctx* c) {
     return BRMQ_OK;
 }
 
+// ------------------------------------------------------------------ shards
+// A split over G devices in contiguous shards; every query's answer is
+// the min over shards of the packed key of its piece on the shard, so one
+// min-allreduce of q keys (NCCL over NVLink, any order) finishes the batch.
+__global__ void k_shard_local(const ulonglong2* __restrict__ Q, uint64_t q, uint64_t off,
+                              uint64_t ns, uint64_t n_total, ulonglong2* __restrict__ Ql,
+                              uint8_t* __restrict__ empty, uint32_t* __restrict__ err) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(Q + i);
+    uint64_t l = x.x, r = x.y;
+    if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
+    if (r >= n_total) atomicOr(err, 1u);                 // naive.hpp:14-15 (whole array)
+    const uint64_t lo = l > off ? l : off;
+    const uint64_t hi = r < off + ns - 1 ? r : off + ns - 1;
+    const bool e = r >= n_total || lo > hi;
+    empty[i] = e;
+    Ql[i] = e ? make_ulonglong2(0, 0) : make_ulonglong2(lo - off, hi - off);
+}
+__global__ void k_shard_keys(const uint64_t* __restrict__ loc, const uint8_t* __restrict__ empty,
+                             const int32_t* __restrict__ A, uint64_t off, uint64_t q,
+                             uint64_t* __restrict__ keys) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    const uint64_t p = loc[i];
+    keys[i] = empty[i] ? ~0ull : brmq::pack_key(__ldg(A + p), uint32_t(off + p));
+}
+
+int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset,
+                          uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
+                          uint64_t* keys, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
+    if (n_total > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    if (n_shard == 0 || offset + n_shard > n_total)
+        return fail(BRMQ_EINVAL, "shard [%llu, %llu) outside the array of %llu",
+                    (unsigned long long)offset, (unsigned long long)(offset + n_shard),
+                    (unsigned long long)n_total);
+    if (q == 0) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    cudaStream_t s = c->stream;
+    // the local solve owns the context workspace: the shard's own buffers are
+    // stream-ordered allocations
+    const size_t a_bytes = (n_shard * 4 + 15) & ~size_t(15);  // keeps the copied queries 16-byte aligned
+    const size_t bytes = q * 16 + q * 8 + q * 8 + q + 96 + (dev ? 0 : a_bytes + q * 16);
+    char* buf = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s));
+    auto* Ql = reinterpret_cast<ulonglong2*>(buf);
+    auto* loc = reinterpret_cast<uint64_t*>(buf + q * 16);
+    auto* dkeys = reinterpret_cast<uint64_t*>(buf + q * 24);
+    auto* empty = reinterpret_cast<uint8_t*>(buf + q * 32);
+    auto* err = reinterpret_cast<uint32_t*>(buf + ((q * 33 + 15) & ~size_t(15)));
+    const int32_t* dA = A;
+    const ulonglong2* dQ = reinterpret_cast<const ulonglong2*>(Q);
+    if (!dev) {
+        auto* hA = reinterpret_cast<int32_t*>(buf + ((q * 33 + 64 + 15) & ~size_t(15)));
+        auto* hQ = reinterpret_cast<ulonglong2*>(reinterpret_cast<char*>(hA) + a_bytes);
+        CUDA_TRY(cudaMemcpyAsync(hA, A, n_shard * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(hQ, Q, q * 16, cudaMemcpyHostToDevice, s));
+        dA = hA;
+        dQ = hQ;
+    }
+    CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
+    const unsigned g = unsigned((q + 255) / 256);
+    k_shard_local<<<g, 256, 0, s>>>(dQ, q, offset, n_shard, n_total, Ql, empty, err);
+    int rc = brmq_solve_bbst(c, dA, n_shard, reinterpret_cast<const brmq_query*>(Ql), q, k, loc,
+                             BRMQ_PTR_DEVICE);
+    if (rc == BRMQ_OK) {
+        k_shard_keys<<<g, 256, 0, s>>>(loc, empty, dA, offset, q, dev ? keys : dkeys);
+        uint32_t herr = 0;
+        if (!dev) CUDA_TRY(cudaMemcpyAsync(keys, dkeys, q * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, err, 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        herr = *reinterpret_cast<uint32_t*>(c->ctl_host);
+        if (herr) rc = fail(BRMQ_ERANGE, "query exceeds array bounds");
+    }
+    cudaFreeAsync(buf, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return rc;
+}
+
 // ------------------------------------------------------------------ naive
 // The harness's "naive" algorithm (naive.hpp:13-21): every query scanned on the
 // device, one warp per query.  A baseline, not a BbST path.
