@@ -196,6 +196,24 @@ inline Answers solve_batch_bbst(std::span<const Value> array, const QueryBatch& 
     return out;
 }
 
+// SPEC.md:331-377 solve_batch_st_rmq_con: the ST-RMQ_CON baseline
+inline Answers solve_batch_st_rmq_con(std::span<const Value> array, const QueryBatch& batch) {
+    Answers out(batch.size());
+    b200::check(brmq_solve_st_rmq_con(b200::context().get(), array.data(), array.size(),
+                                      reinterpret_cast<const brmq_query*>(batch.data()), batch.size(),
+                                      out.data(), BRMQ_PTR_HOST));
+    return out;
+}
+
+// naive.hpp:13-21 for every query (on the device)
+inline Answers solve_batch_naive(std::span<const Value> array, const QueryBatch& batch) {
+    Answers out(batch.size());
+    b200::check(brmq_solve_naive(b200::context().get(), array.data(), array.size(),
+                                 reinterpret_cast<const brmq_query*>(batch.data()), batch.size(),
+                                 out.data(), BRMQ_PTR_HOST));
+    return out;
+}
+
 // SPEC.md:266-310 with a LevelConfig chain (h = 1, or h = 2 with k_1 = 32)
 struct LevelConfig {
     std::vector<std::uint32_t> block_sizes{512};

@@ -34,6 +34,9 @@ int main() {
     CHECK((solve_batch_bbst_con(A, batch, BbstConParams{2, SortKind::Comparison, 4}) == Answers{3, 3}));
     CHECK((solve_batch_bbst(A, batch, 2) == Answers{3, 3}));
     CHECK((solve_batch_bbst(A, batch, LevelConfig{{32, 64}}) == Answers{3, 3}));
+    CHECK((solve_batch_st_rmq_con(A, batch) == Answers{3, 3}));  // SPEC.md:359 worked instance
+    CHECK((solve_batch_st_rmq_con(A, QueryBatch{Query(0, 7)}) == Answers{7}));
+    CHECK((solve_batch_naive(A, batch) == Answers{3, 3}));
     CHECK(floor_log2(48829) == 15);
     bool thrown = false;
     try {
