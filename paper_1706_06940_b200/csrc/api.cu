@@ -6,6 +6,7 @@
 // the device path cannot run the call fails with BRMQ_ECUDA -- there is no CPU
 // fallback anywhere in this library.
 #include <cstdarg>
+#include <cstddef>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -59,10 +60,12 @@ struct Control {
     uint64_t nb;        // |boundary|
     uint64_t aq_len;    // |A_Q|
     uint64_t b_dev;     // blocks over A_Q
-    // boundaries per contraction range (bitmap pipeline) or their exclusive
-    // prefix (radix pipeline / stage API), zeroed with the rest of the block
+    // boundaries per contraction range (bitmap pipeline: k_piece_count) or their
+    // exclusive prefix (radix pipeline / stage API: k_unique); fully rewritten by
+    // every solve, so only the header above is zeroed and copied back
     uint32_t rcnt[brmq::kMaxContractRanges + 1];
 };
+constexpr size_t kCtlHeader = offsetof(Control, rcnt);
 
 }  // namespace
 
@@ -266,7 +269,7 @@ int check_status(brmq_ctx* c) {
 }
 
 int sync_and_read_control(brmq_ctx* c, const Control* ctl_dev) {
-    CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl_dev, sizeof(Control), cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl_dev, kCtlHeader, cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return BRMQ_OK;
@@ -567,7 +570,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -584,7 +587,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
         return BRMQ_OK;
     };
     const GraphKey key{4, A, n, Q, q, 0, 0, answers, s};
@@ -633,7 +636,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -658,7 +661,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
         return BRMQ_OK;
     };
     const GraphKey key{0, A, n, Q, q, k, 0, answers, s};
@@ -714,7 +717,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -739,7 +742,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
         return BRMQ_OK;
     };
     const GraphKey key{2, A, n, Q, q, k, 32, answers, s};
@@ -828,7 +831,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -897,7 +900,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
         return BRMQ_OK;
     };
     const GraphKey key{1, A, n, Q, q, k, sort_kind, answers, s};
@@ -979,7 +982,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -1030,7 +1033,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
         return BRMQ_OK;
     };
     const GraphKey key{3, A, n, Q, q, 1, 0, answers, s};
@@ -1068,7 +1071,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
     auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
-    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
     auto* v = reinterpret_cast<uint32_t*>(P(i_v));
@@ -1149,7 +1152,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     int32_t* dav = dev ? aq_values : reinterpret_cast<int32_t*>(P(i_av));
     uint64_t* dao = dev ? aq_origin : reinterpret_cast<uint64_t*>(P(i_ao));
     uint64_t* dbo = dev ? boundary : reinterpret_cast<uint64_t*>(P(i_bo));
-    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
         CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
@@ -1218,7 +1221,7 @@ int brmq_remap_from_sorted(brmq_ctx* c, const brmq_endpoint* sorted_eps, uint64_
     uint32_t* dcl = dev ? cleft : reinterpret_cast<uint32_t*>(P(i_cl));
     uint32_t* dcr = dev ? cright : reinterpret_cast<uint32_t*>(P(i_cr));
     uint8_t* ddg = dev ? degenerate : reinterpret_cast<uint8_t*>(P(i_dg));
-    CUDA_TRY(cudaMemsetAsync(ctl, 0, sizeof(Control), s));
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
         if (m) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
         if (nb) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dB), boundary, nb * 8, cudaMemcpyHostToDevice, s));
