@@ -153,14 +153,17 @@ __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64
 }
 
 // VPL vectors per lane cover one block (k = 32 * EPV * VPL); TPR ranges per round.
-template <class E, class QP, int VPL, int TPR>
+// WPQ: one warp per query (small batches: the per-warp rounds of partial scans
+// are the latency chain, so spread the queries over 32x more warps).
+template <class E, class QP, int VPL, int TPR, bool WPQ = false>
 __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
                                                     const uint64_t* __restrict__ ST,
                                                     uint64_t stride, uint64_t q,
                                                     uint64_t* __restrict__ answers) {
     const unsigned lane = lane_id();
-    const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x);
-    const bool active = i < q;
+    const uint64_t i = WPQ ? (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5
+                           : (uint64_t(blockIdx.x) * kThreads + threadIdx.x);
+    const bool active = i < q && (!WPQ || lane == 0);
 
     uint64_t best = kNoKey, direct = 0;
     bool done = false, t0 = false, t1 = false;
@@ -253,9 +256,16 @@ __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
     if (active) answers[i] = done ? direct : uint64_t(key_pos(best));
 }
 
+constexpr uint64_t kWarpPerQueryMax = 16384;  // batches up to this size: one warp per query
+
 template <class E, class QP, int VPL, int TPR>
 void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
               uint64_t* ans, cudaStream_t s) {
+    if (q <= kWarpPerQueryMax) {
+        const unsigned grid = unsigned((q * 32 + kThreads - 1) / kThreads);
+        k_query<E, QP, VPL, TPR, true><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans);
+        return;
+    }
     const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
     k_query<E, QP, VPL, TPR><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans);
 }
