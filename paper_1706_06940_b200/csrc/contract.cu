@@ -27,8 +27,8 @@ namespace brmq {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096
+constexpr int kItems = 8;   // 2048-endpoint dedup tiles (measured vs 1024 and 4096)
+constexpr int kTile = kThreads * kItems;
 
 // ------------------------------------------------------------------ collect
 // span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
