@@ -66,6 +66,7 @@ struct Control {
     uint32_t rcnt[brmq::kMaxContractRanges + 1];
 };
 constexpr size_t kCtlHeader = offsetof(Control, rcnt);
+static_assert(kCtlHeader % 4 == 0, "header copied as u32 words");
 
 }  // namespace
 
@@ -95,7 +96,8 @@ struct brmq_ctx {
     size_t st_cap = 0;   // (so stale bytes can never alias a live epoch); zeroed on growth
     uint32_t* bitmap = nullptr;  // persistent, kept all-zero by the contraction kernel
     size_t bitmap_words = 0;
-    Control* ctl_host = nullptr;  // pinned mirror of the control block
+    Control* ctl_host = nullptr;  // pinned, device-mapped mirror of the control header
+    uint32_t* ctl_host_dev = nullptr;  // its device address (solves publish into it)
     uint32_t* epoch_dev = nullptr;  // device epoch counter, bumped by every solve (graph-safe)
     uint32_t epoch_host = 1;        // host mirror of *epoch_dev
     bool use_graphs = true;
@@ -370,7 +372,9 @@ int brmq_ctx_create(brmq_ctx** out, int device) {
         return fail(BRMQ_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
     c->stream = c->own;
-    e = cudaHostAlloc(reinterpret_cast<void**>(&c->ctl_host), sizeof(Control), cudaHostAllocDefault);
+    e = cudaHostAlloc(reinterpret_cast<void**>(&c->ctl_host), sizeof(Control), cudaHostAllocMapped);
+    if (e == cudaSuccess)
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->ctl_host_dev), c->ctl_host, 0);
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->own);
         delete c;
@@ -455,6 +459,13 @@ int brmq_memcpy(brmq_ctx* c, void* dst, const void* src, size_t bytes, int kind)
 int brmq_synchronize(brmq_ctx* c) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return BRMQ_OK;
+}
+
+// The final kernel of a solve copies the control header into the mapped host
+// mirror (no device-to-host copy node in the solve's graph).
+brmq::CtlPublish publish(brmq_ctx* c, Control* ctl) {
+    return brmq::CtlPublish{reinterpret_cast<const uint32_t*>(ctl), c->ctl_host_dev,
+                            &ctl->tickets[4], uint32_t(kCtlHeader / 4)};
 }
 
 // ------------------------------------------------------------------ shards
@@ -578,7 +589,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
             tm.end(0);
         }
         tm.stage("query", launches);
-        const int l = brmq::launch_naive(dA, n, dQ, q, dAns, &ctl->err, s);
+        const int l = brmq::launch_naive(dA, n, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;
@@ -587,7 +598,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
+        // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
     const GraphKey key{4, A, n, Q, q, 0, 0, answers, s};
@@ -652,7 +663,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s);
+        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;
@@ -661,7 +672,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
+        // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
     const GraphKey key{0, A, n, Q, q, k, 0, answers, s};
@@ -733,7 +744,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_ml(dA, n, k, ST, b, SUB, dQ, q, dAns, &ctl->err, s);
+        l = brmq::launch_query_ml(dA, n, k, ST, b, SUB, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;
@@ -742,7 +753,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
+        // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
     const GraphKey key{2, A, n, Q, q, k, 32, answers, s};
@@ -889,9 +900,9 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         tm.stage("query", launches);
         l = use_bitmap ? brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ,
                                                           reinterpret_cast<uint2*>(P(i_wi)), n, q,
-                                                          dAns, s)
+                                                          dAns, s, publish(c, ctl))
                        : brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr,
-                                                       q, dAns, s);
+                                                       q, dAns, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;
@@ -900,7 +911,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
+        // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
     const GraphKey key{1, A, n, Q, q, k, sort_kind, answers, s};
@@ -1024,7 +1035,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_st(dQ, cl, cr, q, ST, e_max, dAns, s);
+        l = brmq::launch_query_st(dQ, cl, cr, q, ST, e_max, dAns, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;
@@ -1033,7 +1044,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
             CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
             tm.end(0);
         }
-        CUDA_TRY(cudaMemcpyAsync(c->ctl_host, ctl, kCtlHeader, cudaMemcpyDeviceToHost, s));
+        // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
     const GraphKey key{3, A, n, Q, q, 1, 0, answers, s};

@@ -8,6 +8,8 @@
 // Valid because positions fit 32 bits (n <= 2^32-1, contraction.hpp:13).
 #pragma once
 
+#include "kernels.h"  // CtlPublish
+
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -181,6 +183,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait_sleep(bar, parity)) {
     }
 }
+// The end of a solve: the last CTA of its final kernel copies the control header
+// (errors, sizes) into host-mapped pinned memory, so no device-to-host copy node
+// follows the kernels (a copy node cost ~7 us per solve on this part).
+__device__ __forceinline__ void publish_control(const CtlPublish& p) {
+    if (!p.host) return;
+    __shared__ bool s_last_cta;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's writes (err bits) before its ticket
+        s_last_cta = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last_cta) return;
+    __threadfence();
+    for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) p.host[i] = __ldcg(p.ctl + i);
+    __threadfence_system();
+}
+
 __device__ __forceinline__ uint32_t ld_volatile_shared_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");

@@ -347,12 +347,11 @@ __global__ void k_marked_edges(const int32_t* __restrict__ A, uint64_t n,
 
 // Query i: [2 cl + 1, 2 cr + 1] in E through the element Sparse Table (row e at
 // ST + e * stride), the two-range trick of element_sparse_table.cpp:35-44.
-__global__ void k_query_st(const ulonglong2* __restrict__ Q, const uint32_t* __restrict__ cleft,
-                           const uint32_t* __restrict__ cright_raw, uint64_t q,
-                           const uint64_t* __restrict__ ST, uint64_t stride,
-                           uint64_t* __restrict__ answers) {
-    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= q) return;
+__device__ __forceinline__ void st_one(const ulonglong2* __restrict__ Q,
+                                       const uint32_t* __restrict__ cleft,
+                                       const uint32_t* __restrict__ cright_raw, uint64_t i,
+                                       const uint64_t* __restrict__ ST, uint64_t stride,
+                                       uint64_t* __restrict__ answers) {
     const ulonglong2 x = __ldg(Q + i);
     const uint64_t l = x.x < x.y ? x.x : x.y;
     const uint64_t il = 2 * uint64_t(__ldg(cleft + i)) + 1, ir = 2 * uint64_t(__ldg(cright_raw + i)) + 1;
@@ -363,6 +362,14 @@ __global__ void k_query_st(const ulonglong2* __restrict__ Q, const uint32_t* __r
     const uint32_t e = floor_log2_u64(ir - il + 1);
     const uint64_t* row = ST + uint64_t(e) * stride;
     answers[i] = key_pos(kmin(__ldg(row + il), __ldg(row + ir + 1 - (1ull << e))));
+}
+__global__ void k_query_st(const ulonglong2* __restrict__ Q, const uint32_t* __restrict__ cleft,
+                           const uint32_t* __restrict__ cright_raw, uint64_t q,
+                           const uint64_t* __restrict__ ST, uint64_t stride,
+                           uint64_t* __restrict__ answers, const CtlPublish pub) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < q) st_one(Q, cleft, cright_raw, i, ST, stride, answers);
+    publish_control(pub);
 }
 
 inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
@@ -463,10 +470,10 @@ int launch_marked_edges(const int32_t* A, uint64_t n, const uint32_t* span, cons
 
 int launch_query_st(const uint64_t* Q, const uint32_t* cleft, const uint32_t* cright_raw,
                     uint64_t q, const uint64_t* ST, uint64_t stride, uint64_t* answers,
-                    cudaStream_t s) {
+                    cudaStream_t s, const CtlPublish& pub) {
     if (!q) return 0;
     k_query_st<<<g256(q), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), cleft, cright_raw,
-                                        q, ST, stride, answers);
+                                        q, ST, stride, answers, pub);
     return 1;
 }
 

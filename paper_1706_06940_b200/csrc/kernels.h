@@ -10,6 +10,15 @@
 
 namespace brmq {
 
+// End-of-solve publication of the control header into host-mapped memory by the
+// last CTA of the final kernel (common.cuh publish_control); host == nullptr: off.
+struct CtlPublish {
+    const uint32_t* ctl;  // device control header (u32 words)
+    uint32_t* host;       // host-mapped mirror
+    uint32_t* ticket;     // zeroed with the header at solve start
+    uint32_t words;
+};
+
 // ---------------------------------------------------------------- block_argmin.cu
 // Level 0 of the block Sparse Table: keys[j] = packed leftmost-min key of block j
 // (SPEC.md:199-203).
@@ -32,23 +41,28 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
 
 // ---------------------------------------------------------------- query.cu
 int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
-                 uint32_t* err, cudaStream_t stream);
+                 uint32_t* err, cudaStream_t stream,
+                    const CtlPublish& pub = CtlPublish{});
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST,
                         uint64_t b, const uint64_t* Q, uint64_t q, uint64_t* answers,
-                        uint32_t* err, cudaStream_t stream);
+                        uint32_t* err, cudaStream_t stream,
+                    const CtlPublish& pub = CtlPublish{});
 // Multi-level BbST [32, k] answering: endpoint blocks resolved through the
 // 32-element sub-block keys, raw A read only inside partial sub-blocks.
 int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                     const uint64_t* sub, const uint64_t* Q, uint64_t q, uint64_t* answers,
-                    uint32_t* err, cudaStream_t stream);
+                    uint32_t* err, cudaStream_t stream,
+                    const CtlPublish& pub = CtlPublish{});
 // bitmap pipeline: contracted coordinates from the contraction's word_info
 int launch_query_contracted_wi(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
                                const uint64_t* Q, const uint2* word_info, uint64_t n, uint64_t q,
-                               uint64_t* answers, cudaStream_t stream);
+                               uint64_t* answers, cudaStream_t stream,
+                    const CtlPublish& pub = CtlPublish{});
 int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint32_t k,
                             const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
                             const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,
-                            uint64_t* answers, cudaStream_t stream);
+                            uint64_t* answers, cudaStream_t stream,
+                    const CtlPublish& pub = CtlPublish{});
 
 // ---------------------------------------------------------------- radix_sort.cu
 size_t radix_sort_temp_bytes(uint64_t m, int bits);     // zeroed scratch (histograms, tickets)
@@ -117,6 +131,7 @@ int launch_marked_edges(const int32_t* A, uint64_t n, const uint32_t* span, cons
                         uint64_t* E, cudaStream_t s);
 int launch_query_st(const uint64_t* Q, const uint32_t* cleft, const uint32_t* cright_raw,
                     uint64_t q, const uint64_t* ST, uint64_t stride, uint64_t* answers,
-                    cudaStream_t s);
+                    cudaStream_t s,
+                    const CtlPublish& pub = CtlPublish{});
 
 }  // namespace brmq

@@ -159,7 +159,8 @@ template <class E, class QP, int VPL, int TPR, bool WPQ = false>
 __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
                                                     const uint64_t* __restrict__ ST,
                                                     uint64_t stride, uint64_t q,
-                                                    uint64_t* __restrict__ answers) {
+                                                    uint64_t* __restrict__ answers,
+                                                    const CtlPublish pub) {
     const unsigned lane = lane_id();
     const uint64_t i = WPQ ? (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5
                            : (uint64_t(blockIdx.x) * kThreads + threadIdx.x);
@@ -254,55 +255,53 @@ __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
         }
     }
     if (active) answers[i] = done ? direct : uint64_t(key_pos(best));
+    publish_control(pub);
 }
 
 constexpr uint64_t kWarpPerQueryMax = 16384;  // batches up to this size: one warp per query
 
 template <class E, class QP, int VPL, int TPR>
 void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
-              uint64_t* ans, cudaStream_t s) {
+              uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
     if (q <= kWarpPerQueryMax) {
         const unsigned grid = unsigned((q * 32 + kThreads - 1) / kThreads);
-        k_query<E, QP, VPL, TPR, true><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans);
+        k_query<E, QP, VPL, TPR, true><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans, pub);
         return;
     }
     const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
-    k_query<E, QP, VPL, TPR><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans);
+    k_query<E, QP, VPL, TPR><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans, pub);
 }
 
 template <class QP>
 void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
-                  uint64_t* ans, cudaStream_t s) {
+                  uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
     const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0;
     // one pending range per round: fewer registers -> more resident warps, which
     // beats batching ranges per round on this latency-bound kernel (measured)
-    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 4>(e, qp, k, ST, stride, q, ans, s);
-    return launch_q<ElemI32, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
+    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 4>(e, qp, k, ST, stride, q, ans, s, pub);
+    return launch_q<ElemI32, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s, pub);
 }
 
 template <class QP>
 void dispatch_key(ElemKey e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
-                  uint64_t* ans, cudaStream_t s) {
-    if (k == 512) return launch_q<ElemKey, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (k == 256) return launch_q<ElemKey, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (k == 1024) return launch_q<ElemKey, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s);
-    if (k == 128) return launch_q<ElemKey, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s);
-    return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s);
+                  uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
+    if (k == 512) return launch_q<ElemKey, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (k == 256) return launch_q<ElemKey, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (k == 1024) return launch_q<ElemKey, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (k == 128) return launch_q<ElemKey, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s, pub);
+    return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s, pub);
 }
 
 // The harness's "naive" algorithm (naive.hpp:13-21 on the device): one warp per
 // query scans A[l..r]; lanes take strided elements, a redux pair keeps the
 // leftmost minimum.
-__global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ A, uint64_t n,
-                                                    const ulonglong2* __restrict__ Q, uint64_t q,
-                                                    uint64_t* __restrict__ answers,
-                                                    uint32_t* __restrict__ err) {
-    const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    if (i >= q) return;
+__device__ __forceinline__ void naive_one(const int32_t* __restrict__ A, uint64_t n,
+                                          const ulonglong2* __restrict__ Q, uint64_t i,
+                                          uint64_t* __restrict__ answers, uint32_t* __restrict__ err) {
     const ulonglong2 x = __ldg(Q + i);
     uint64_t l = x.x, r = x.y;
     if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
@@ -319,39 +318,49 @@ __global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ 
     if (lane_id() == 0) answers[i] = key_pos(b);
 }
 
+__global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ A, uint64_t n,
+                                                    const ulonglong2* __restrict__ Q, uint64_t q,
+                                                    uint64_t* __restrict__ answers,
+                                                    uint32_t* __restrict__ err, const CtlPublish pub) {
+    const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (i < q) naive_one(A, n, Q, i, answers, err);
+    publish_control(pub);
+}
+
 }  // namespace
 
 int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
-                 uint32_t* err, cudaStream_t stream) {
+                 uint32_t* err, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
     k_naive<<<unsigned((q * 32 + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
-        A, n, reinterpret_cast<const ulonglong2*>(Q), q, answers, err);
+        A, n, reinterpret_cast<const ulonglong2*>(Q), q, answers, err, pub);
     return 1;
 }
 
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                         const uint64_t* Q, uint64_t q, uint64_t* answers, uint32_t* err,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
-    dispatch_i32(ElemI32{A, n}, QueryDirect{Q, n, err}, k, ST, b, q, answers, stream);
+    dispatch_i32(ElemI32{A, n}, QueryDirect{Q, n, err}, k, ST, b, q, answers, stream, pub);
     return 1;
 }
 
 int launch_query_contracted_wi(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
                                const uint64_t* Q, const uint2* word_info, uint64_t n, uint64_t q,
-                               uint64_t* answers, cudaStream_t stream) {
+                               uint64_t* answers, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
-    dispatch_key(ElemKey{AQ}, QueryContractedWI{Q, word_info, n}, k, ST, b_max, q, answers, stream);
+    dispatch_key(ElemKey{AQ}, QueryContractedWI{Q, word_info, n}, k, ST, b_max, q, answers, stream,
+                 pub);
     return 1;
 }
 
 int launch_query_contracted(const uint64_t* AQ, const uint64_t* /*aq_len_dev*/, uint32_t k,
                             const uint64_t* ST, uint64_t b_max, const uint64_t* Q,
                             const uint32_t* cleft, const uint32_t* cright_raw, uint64_t q,
-                            uint64_t* answers, cudaStream_t stream) {
+                            uint64_t* answers, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
     dispatch_key(ElemKey{AQ}, QueryContracted{Q, cleft, cright_raw}, k, ST, b_max, q, answers,
-                 stream);
+                 stream, pub);
     return 1;
 }
 
@@ -430,15 +439,11 @@ __device__ __noinline__ uint64_t resolve_sub(const int32_t* __restrict__ A, uint
 }
 
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict__ A, uint64_t n,
-                                                       uint32_t k, const uint64_t* __restrict__ ST,
-                                                       uint64_t stride,
-                                                       const uint64_t* __restrict__ sub,
-                                                       const uint64_t* __restrict__ Q, uint64_t q,
-                                                       uint64_t* __restrict__ answers,
-                                                       uint32_t* __restrict__ err) {
-    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
-    if (i >= q) return;
+__device__ __forceinline__ void ml_one(const int32_t* __restrict__ A, uint64_t n, uint32_t k,
+                                       const uint64_t* __restrict__ ST, uint64_t stride,
+                                       const uint64_t* __restrict__ sub,
+                                       const uint64_t* __restrict__ Q, uint64_t i,
+                                       uint64_t* __restrict__ answers, uint32_t* __restrict__ err) {
     const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
     uint64_t l = x.x, r = x.y;
     if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
@@ -478,17 +483,31 @@ __global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict
     answers[i] = key_pos(best);
 }
 
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict__ A, uint64_t n,
+                                                       uint32_t k, const uint64_t* __restrict__ ST,
+                                                       uint64_t stride,
+                                                       const uint64_t* __restrict__ sub,
+                                                       const uint64_t* __restrict__ Q, uint64_t q,
+                                                       uint64_t* __restrict__ answers,
+                                                       uint32_t* __restrict__ err,
+                                                       const CtlPublish pub) {
+    const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (i < q) ml_one<VEC>(A, n, k, ST, stride, sub, Q, i, answers, err);
+    publish_control(pub);
+}
+
 }  // namespace
 
 int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                     const uint64_t* sub, const uint64_t* Q, uint64_t q, uint64_t* answers,
-                    uint32_t* err, cudaStream_t stream) {
+                    uint32_t* err, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
     const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
     if ((reinterpret_cast<uintptr_t>(A) & 15u) == 0)
-        k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err);
+        k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
     else
-        k_query_ml<false><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err);
+        k_query_ml<false><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
     return 1;
 }
 
