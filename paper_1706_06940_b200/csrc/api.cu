@@ -98,6 +98,7 @@ struct brmq_ctx {
     size_t bitmap_words = 0;
     Control* ctl_host = nullptr;  // pinned, device-mapped mirror of the control header
     uint32_t* ctl_host_dev = nullptr;  // its device address (solves publish into it)
+    bool ctl_clean = false;  // the device control header is all-zero (no memset needed)
     uint32_t* epoch_dev = nullptr;  // device epoch counter, bumped by every solve (graph-safe)
     uint32_t epoch_host = 1;        // host mirror of *epoch_dev
     bool use_graphs = true;
@@ -156,6 +157,7 @@ int ensure_ws(brmq_ctx* c, size_t bytes) {
     CUDA_TRY(cudaMalloc(&c->ws, cap));
     CUDA_TRY(cudaMemsetAsync(c->ws, 0, cap, c->stream));
     c->ws_cap = cap;
+    c->ctl_clean = true;
     return BRMQ_OK;
 }
 
@@ -463,9 +465,19 @@ int brmq_synchronize(brmq_ctx* c) {
 
 // The final kernel of a solve copies the control header into the mapped host
 // mirror (no device-to-host copy node in the solve's graph).
+// The final kernel also re-zeroes the accumulating fields (err, span, tickets) for
+// the next solve, so a solve's graph needs no memset node; prepare_ctl zeroes the
+// header explicitly (outside any graph) only when something else left it dirty.
 brmq::CtlPublish publish(brmq_ctx* c, Control* ctl) {
     return brmq::CtlPublish{reinterpret_cast<const uint32_t*>(ctl), c->ctl_host_dev,
-                            &ctl->tickets[4], uint32_t(kCtlHeader / 4)};
+                            &ctl->tickets[4], uint32_t(kCtlHeader / 4),
+                            uint32_t(offsetof(Control, nb) / 4)};
+}
+
+int prepare_ctl(brmq_ctx* c, Control* ctl) {
+    if (!c->ctl_clean) CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, c->stream));
+    c->ctl_clean = false;  // until this solve's final kernel has run
+    return BRMQ_OK;
 }
 
 // ------------------------------------------------------------------ shards
@@ -581,7 +593,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+        // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -602,7 +614,9 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
         return BRMQ_OK;
     };
     const GraphKey key{4, A, n, Q, q, 0, 0, answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     c->info.kernel_launches = uint32_t(launches);
@@ -647,7 +661,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+        // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -676,7 +690,9 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         return BRMQ_OK;
     };
     const GraphKey key{0, A, n, Q, q, k, 0, answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     c->info.blocks = b;
@@ -728,7 +744,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+        // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -757,7 +773,9 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         return BRMQ_OK;
     };
     const GraphKey key{2, A, n, Q, q, k, 32, answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
     c->info.blocks = b;
@@ -842,7 +860,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+        // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -915,7 +933,9 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         return BRMQ_OK;
     };
     const GraphKey key{1, A, n, Q, q, k, sort_kind, answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     c->epoch_host += n_epochs;
     CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
@@ -993,7 +1013,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     int launches = 0;
     auto enqueue = [&]() -> int {
         int l = 0;
-        CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+        // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
             CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -1048,7 +1068,9 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         return BRMQ_OK;
     };
     const GraphKey key{3, A, n, Q, q, 1, 0, answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     c->epoch_host += n_epochs;
     CUDA_TRY(cudaStreamSynchronize(s));
     tm.finish();
@@ -1082,6 +1104,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
     auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
+    c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
@@ -1105,6 +1128,7 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
     const size_t i_rs = cv.add(brmq::radix_sort_temp_bytes(m, 32));
     const size_t i_e = dev ? 0 : cv.add(m * 8);
     if (int rc = ensure_ws(c, cv.total)) return rc;
+    c->ctl_clean = false;  // stage calls may overwrite the control header
     if (int rc = ensure_status(c, brmq::radix_sort_status_words(m, 32) * 8)) return rc;
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
     cudaStream_t s = c->stream;
@@ -1163,6 +1187,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     int32_t* dav = dev ? aq_values : reinterpret_cast<int32_t*>(P(i_av));
     uint64_t* dao = dev ? aq_origin : reinterpret_cast<uint64_t*>(P(i_ao));
     uint64_t* dbo = dev ? boundary : reinterpret_cast<uint64_t*>(P(i_bo));
+    c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
         CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
@@ -1232,6 +1257,7 @@ int brmq_remap_from_sorted(brmq_ctx* c, const brmq_endpoint* sorted_eps, uint64_
     uint32_t* dcl = dev ? cleft : reinterpret_cast<uint32_t*>(P(i_cl));
     uint32_t* dcr = dev ? cright : reinterpret_cast<uint32_t*>(P(i_cr));
     uint8_t* ddg = dev ? degenerate : reinterpret_cast<uint8_t*>(P(i_dg));
+    c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
         if (m) CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
@@ -1271,6 +1297,7 @@ int brmq_build_block_sparse(brmq_ctx* c, const int32_t* values, uint64_t m, uint
     const size_t i_v = dev ? 0 : cv.add(m * 4);
     const size_t i_t = dev ? 0 : cv.add(cells * 8);
     if (int rc = ensure_ws(c, cv.total)) return rc;
+    c->ctl_clean = false;  // stage calls may overwrite the control header
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
     cudaStream_t s = c->stream;
     const int32_t* dV = dev ? values : reinterpret_cast<int32_t*>(P(i_v));

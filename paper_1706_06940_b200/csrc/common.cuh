@@ -198,6 +198,9 @@ __device__ __forceinline__ void publish_control(const CtlPublish& p) {
     if (!s_last_cta) return;
     __threadfence();
     for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) p.host[i] = __ldcg(p.ctl + i);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < p.reset_words; i += blockDim.x)
+        const_cast<uint32_t*>(p.ctl)[i] = 0u;
     __threadfence_system();
 }
 

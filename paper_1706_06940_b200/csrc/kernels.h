@@ -17,6 +17,7 @@ struct CtlPublish {
     uint32_t* host;       // host-mapped mirror
     uint32_t* ticket;     // zeroed with the header at solve start
     uint32_t words;
+    uint32_t reset_words; // leading words re-zeroed after the copy (for the next solve)
 };
 
 // ---------------------------------------------------------------- block_argmin.cu

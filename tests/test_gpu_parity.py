@@ -329,3 +329,26 @@ def test_workspace_reuse_sequence(engine, orc):
         for variant in VARIANTS:
             got = _solve(engine, variant, A, Q, 512)
             assert np.array_equal(got, want), (q, variant, np.nonzero(got != want)[0][:5])
+
+
+def test_control_block_protocol(engine, orc):
+    """Solves leave the device control header zeroed for the next solve (no memset
+    in their graphs); stage calls and failed solves leave it dirty and the next
+    solve must re-zero it.  Interleave them all and check every answer."""
+    r = np.random.default_rng(2024)
+    n = 400_000
+    A = _values(r, n, "ties16")
+    Qs = [_queries(r, n, q, kind) for q, kind in ((5000, "uniform"), (70_000, "mixed"), (300, "short"))]
+    wants = [orc.solve_oracle(A, Q) for Q in Qs]
+    eps = engine.collect_endpoints(Qs[0])
+    for rep in range(2):
+        for Q, want in zip(Qs, wants):
+            for variant in VARIANTS:
+                assert np.array_equal(_solve(engine, variant, A, Q, 512), want), (rep, variant)
+            engine.sort_endpoints(eps.copy())  # stage call: header dirty
+            assert np.array_equal(_solve(engine, "con_bitmap", A, Q, 512), want)
+            with pytest.raises(OutOfRange):  # failed solve
+                engine.solve_batch_bbst_con(A, make_queries([0], [n]), 512, SortKind.Bitmap)
+            assert np.array_equal(_solve(engine, "con_radix", A, Q, 512), want)
+            engine.build_block_sparse(A[:1000], 8)  # stage call
+            assert np.array_equal(_solve(engine, "bbst", A, Q, 512), want)
