@@ -871,7 +871,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
-            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap, nullptr, R,
+            l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap,
                                      ctl->span, &ctl->err, s, c->epoch_dev, n_epochs);
             l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
             launches += l;
@@ -882,7 +882,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
             auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
             tm.stage("collect", launches);
-            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s,
+            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s,
                                      c->epoch_dev, n_epochs);
             launches += l;
             tm.end(l);
@@ -1026,7 +1026,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
         auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
         tm.stage("collect", launches);
-        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, 0, nullptr, &ctl->err, s,
+        l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s,
                                  c->epoch_dev, n_epochs);
         launches += l;
         tm.end(l);
@@ -1109,7 +1109,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
     if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
     auto* v = reinterpret_cast<uint32_t*>(P(i_v));
-    brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, 0, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
+    brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
     brmq::launch_join_eps(k, v, m, dE, s);
     if (int rc = check_status(c)) return rc;
     if (!dev) CUDA_TRY(cudaMemcpyAsync(eps, dE, m * 8, cudaMemcpyDeviceToHost, s));

@@ -33,26 +33,20 @@ constexpr int kTile = kThreads * kItems;
 // ------------------------------------------------------------------ collect
 // span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
 // Grid-stride with a capped grid so the span needs only 2 atomics per CTA.
-// With a bitmap, also counts the distinct positions of every contraction range
-// (range = (pos >> kContractTileLog2) / R) into rcnt[G]: a bit that the
-// atomicOr newly set is a new boundary.  Counted in a shared histogram first,
-// so the global counters see one add per (CTA, range).
+// With a bitmap, marks every endpoint with a fire-and-forget reduction (the
+// boundaries per contraction piece are popcounted afterwards: k_piece_count).
 __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restrict__ Q, uint64_t q,
                                                       uint64_t n, uint32_t* __restrict__ keys,
                                                       uint32_t* __restrict__ vals,
                                                       uint32_t* __restrict__ bitmap,
-                                                      uint32_t* __restrict__ rcnt, uint32_t R,
-                                                      uint32_t G, uint32_t* __restrict__ span,
+                                                      uint32_t* __restrict__ span,
                                                       uint32_t* __restrict__ err,
                                                       uint32_t* __restrict__ epoch_bump,
                                                       uint32_t epoch_by) {
     // the solve's epoch reservation rides on this first kernel (no extra launch)
     if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) *epoch_bump += epoch_by;
     __shared__ uint32_t s_lo, s_hi;
-    __shared__ uint32_t s_hist[kMaxContractRanges];
     if (threadIdx.x == 0) { s_lo = 0xFFFFFFFFu; s_hi = 0; }
-    if (bitmap && rcnt)
-        for (uint32_t j = threadIdx.x; j < G; j += kThreads) s_hist[j] = 0;
     __syncthreads();
     uint32_t lo_acc = 0xFFFFFFFFu, hi_acc = 0;
     const uint64_t stride = uint64_t(gridDim.x) * kThreads;
@@ -72,24 +66,11 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                 make_uint2(uint32_t(i << 1), uint32_t((i << 1) | 1u));  // contraction.hpp:16-18
         }
         if (bitmap) {
-            const uint32_t bl = 1u << (lo & 31), bh = 1u << (hi & 31);
-            if (rcnt) {
-                if (!(atomicOr(bitmap + (lo >> 5), bl) & bl))
-                    atomicAdd(s_hist + (lo >> kContractTileLog2) / R, 1u);
-                if (!(atomicOr(bitmap + (hi >> 5), bh) & bh))
-                    atomicAdd(s_hist + (hi >> kContractTileLog2) / R, 1u);
-            } else {  // marks only (fire-and-forget reductions); counted by k_piece_count (contraction.cu)
-                atomicOr(bitmap + (lo >> 5), bl);
-                atomicOr(bitmap + (hi >> 5), bh);
-            }
+            atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
+            atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
         }
         lo_acc = lo < lo_acc ? lo : lo_acc;
         hi_acc = hi > hi_acc ? hi : hi_acc;
-    }
-    if (bitmap && rcnt) {
-        __syncthreads();
-        for (uint32_t j = threadIdx.x; j < G; j += kThreads)
-            if (s_hist[j]) atomicAdd(rcnt + j, s_hist[j]);
     }
     if (span) {
         const uint32_t wlo = __reduce_min_sync(kFull, lo_acc);
@@ -378,16 +359,13 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 
 // ------------------------------------------------------------------ launchers
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
-                   uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
-                   uint32_t* err, cudaStream_t s, uint32_t* epoch_bump, uint32_t epoch_by) {
+                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
+                   uint32_t* epoch_bump, uint32_t epoch_by) {
     if (q == 0) return 0;
     const unsigned cap = 148u * 16u;
     const unsigned grid = g256(q) < cap ? g256(q) : cap;
-    uint32_t G = 0, R = 1;
-    if (bitmap) contract_partition(n, &G, &R);
-    if (bitmap && R != range_tiles) return -1;  // caller and kernel disagree on the partition
     k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
-                                           bitmap, rcnt, R, G, span, err, epoch_bump, epoch_by);
+                                           bitmap, span, err, epoch_bump, epoch_by);
     return 1;
 }
 

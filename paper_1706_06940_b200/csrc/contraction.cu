@@ -28,9 +28,10 @@
 //     redux.min and a one-load leftmost search; rows holding boundaries are
 //     closed cooperatively by the warp (sparse) or each by its lane (dense);
 //   - the open segment and the running rank are carried in registers.
-// Rank bases: the endpoint stage counted the boundaries of every range (or
-// wrote their prefix) while marking the bitmap, and each warp popcounts its
-// own piece of the bitmap while its first loads are in flight.
+// Rank bases: per range, the boundary counts k_piece_count popcounted from the
+// bitmap (bitmap pipeline) or the exclusive prefix k_unique wrote (sorted
+// endpoints); per warp, the piece counts of k_piece_count or, with the prefix,
+// a popcount of the warp's own piece while its first loads are in flight.
 // Stitch: every warp publishes (tail of its piece, has-boundary); the area
 // closed by a warp's first boundary folds the tails of the pieces before it
 // back to the nearest piece holding a boundary -- in the CTA through shared

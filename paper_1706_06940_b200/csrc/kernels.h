@@ -78,16 +78,15 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
 
 // ---------------------------------------------------------------- contract.cu
 // The contraction partitions the tiles of A into G ranges of R tiles
-// (contract_partition); the endpoint stage counts the distinct boundaries of
-// each range into rcnt[G] (zeroed by the caller) while it marks the bitmap
-// (k_collect), or -- from sorted endpoints (k_unique) -- writes the exclusive
-// prefix rfirst[0..G] directly; launch_contract's `prefix` says which.
+// (contract_partition).  Its rank bases come either from the marked bitmap
+// (k_collect, then k_piece_count: boundaries per piece and per range) or -- from
+// sorted endpoints (k_unique) -- from the exclusive prefix rfirst[0..G] of the
+// boundaries per range; launch_contract's `prefix` says which.
 constexpr uint32_t kMaxContractRanges = 2048;
 constexpr int kContractTileLog2 = 12;  // 4096-position tiles
 void contract_partition(uint64_t n, uint32_t* G, uint32_t* R);
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
-                   uint32_t* bitmap, uint32_t* rcnt, uint32_t range_tiles, uint32_t* span,
-                   uint32_t* err, cudaStream_t s,
+                   uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
 // Boundaries per contraction piece (pcnt[g * 8 + w], 8 warps per range) and per
 // range (rcnt[g]), popcounted from the bitmap.
