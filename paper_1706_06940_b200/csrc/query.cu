@@ -1,3 +1,4 @@
+#include <cstdlib>
 // query.cu -- speculative query answering over the block Sparse Table (K3).
 //
 // SPEC.md:219-236 (inner_span_min + answer_one), PAPER.md:242-255 (BbST_CON
@@ -94,7 +95,7 @@ struct QueryDirect {
     uint64_t n;
     uint32_t* err;
     __device__ __forceinline__ Resolved resolve(uint64_t i) const {
-        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(Q) + i);  // streamed
         uint64_t l = x.x, r = x.y;
         if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
         Resolved o{l, r, l, r, 0, false};
@@ -115,7 +116,7 @@ struct QueryContracted {
     const uint32_t* cleft;
     const uint32_t* cright_raw;
     __device__ __forceinline__ Resolved resolve(uint64_t i) const {
-        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(Q) + i);  // streamed
         uint64_t l = x.x, r = x.y;
         if (l > r) { const uint64_t t = l; l = r; r = t; }
         const uint32_t cl = __ldg(cleft + i), cr = __ldg(cright_raw + i);
@@ -133,7 +134,7 @@ struct QueryContractedWI {
     const uint2* word_info;
     uint64_t n;
     __device__ __forceinline__ Resolved resolve(uint64_t i) const {
-        const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(Q) + i);
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(Q) + i);  // streamed
         uint64_t l = x.x, r = x.y;
         if (l > r) { const uint64_t t = l; l = r; r = t; }
         if (r >= n) { r = n - 1; if (l > r) l = r; }  // already reported by the endpoint stage
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
             }
         }
     }
-    if (active) answers[i] = done ? direct : uint64_t(key_pos(best));
+    if (active) __stcs(reinterpret_cast<unsigned long long*>(answers + i), (unsigned long long)(done ? direct : uint64_t(key_pos(best))));
     publish_control(pub);
 }
 
@@ -497,6 +498,214 @@ __global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict
     publish_control(pub);
 }
 
+// ---- flat variant: power-of-two k <= 512 (<= 16 sub-blocks per block) --------
+// ncu on c3 showed the lane-private resolution above at 4.9 active threads per
+// issued instruction: the lanes that must descend (a third of the queries) run
+// their variable-length sub-key loops and row scans one after another while
+// the rest idle.  Here the descent has a FIXED shape, so a warp issues it once
+// for all its lanes:
+//   - a side [lo, hi] (inside one k-block) is resolved lane-privately from the
+//     block's sub-block keys -- one 128-byte line for k = 512, loaded as 8
+//     predicated 16-byte vectors -- plus its two edge keys;
+//   - the partial edge rows that survive (their exact bound is below the
+//     running best) are pooled per warp and scanned by HALF-warps, one
+//     coalesced 8-byte load per lane per row, a batch of rows in flight at once.
+// Same speculation and bounds as ml_one / resolve_sub; all shifts, no division.
+constexpr int kMlBatch = 4;  // rows per half-warp per batch
+
+// minimum key over the calling lane's half-warp (both halves at once)
+__device__ __forceinline__ uint64_t half_min_key(uint64_t k, bool upper) {
+    const uint32_t hi = key_hi(k), lo = key_pos(k);
+    const uint32_t h0 = __reduce_min_sync(kFull, upper ? 0xFFFFFFFFu : hi);
+    const uint32_t h1 = __reduce_min_sync(kFull, upper ? hi : 0xFFFFFFFFu);
+    const uint32_t mh = upper ? h1 : h0;
+    const uint32_t p0 = __reduce_min_sync(kFull, (!upper && hi == mh) ? lo : 0xFFFFFFFFu);
+    const uint32_t p1 = __reduce_min_sync(kFull, (upper && hi == mh) ? lo : 0xFFFFFFFFu);
+    return (uint64_t(mh) << 32) | (upper ? p1 : p0);
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+    const uint32_t a = __shfl_sync(kFull, uint32_t(v), src);
+    const uint32_t b = __shfl_sync(kFull, uint32_t(v >> 32), src);
+    return (uint64_t(b) << 32) | a;
+}
+
+// One partial edge row: A[lo..hi] inside one 32-aligned row, scanned only if
+// pack(v, lo) (v = the stored minimum of its sub-block, which lies outside the
+// row part) is below the owner's best.
+struct RowTask {
+    uint32_t lo, hi, v;
+    bool need;
+};
+
+// Side [lo, hi] (act: this lane has the side) against the block's sub-block
+// keys: the minimum over the covered sub-blocks whose key lies inside, and the
+// edge rows left to scan.  ks = log2(k / 32).
+__device__ __forceinline__ uint64_t side_flat(const uint64_t* __restrict__ sub, bool act, uint32_t lo,
+                                              uint32_t hi, uint32_t ks, RowTask& rl, RowTask& rr) {
+    const uint32_t sl = lo >> 5, sr = hi >> 5, sb = (sl >> ks) << ks, K = 1u << ks;
+    const ulonglong2* sub2 = reinterpret_cast<const ulonglong2*>(sub + sb);
+    ulonglong2 x[8];
+#pragma unroll
+    for (uint32_t c = 0; c < 8; ++c) {
+        const uint32_t s = sb + 2 * c;
+        x[c] = (act && 2 * c < K && s + 1 > sl && s < sr) ? __ldg(sub2 + c) : make_ulonglong2(kNoKey, kNoKey);
+    }
+    const uint64_t kl = act ? __ldg(sub + sl) : kNoKey, kr = act ? __ldg(sub + sr) : kNoKey;
+    uint64_t cand = kNoKey;
+#pragma unroll
+    for (uint32_t c = 0; c < 8; ++c) {  // interior sub-blocks (sl, sr)
+        const uint32_t s = sb + 2 * c;
+        if (s > sl && s < sr) cand = kmin(cand, x[c].x);
+        if (s + 1 > sl && s + 1 < sr) cand = kmin(cand, x[c].y);
+    }
+    rl.need = rr.need = false;
+    if (act) {
+        if (key_pos(kl) >= lo && key_pos(kl) <= hi) cand = kmin(cand, kl);
+        else rl = RowTask{lo, sl == sr ? hi : (sl << 5) + 31, key_hi(kl), true};
+        if (sr != sl) {
+            if (key_pos(kr) <= hi) cand = kmin(cand, kr);
+            else rr = RowTask{sr << 5, hi, key_hi(kr), true};
+        }
+    }
+    return cand;
+}
+
+// One warp answers queries [g * 32, g * 32 + 32) (lane = query).
+template <bool VEC>
+__device__ __forceinline__ void ml_flat_group(
+    const int32_t* __restrict__ A, uint64_t n, uint32_t kshift, const uint64_t* __restrict__ ST,
+    uint64_t stride, const uint64_t* __restrict__ sub, const uint64_t* __restrict__ Q, uint64_t q,
+    uint64_t* __restrict__ answers, uint32_t* __restrict__ err, uint64_t g, uint4* s_rows) {
+    const uint32_t lane = lane_id();
+    const bool upper = lane >= 16;
+    const uint32_t j = lane & 15u;
+    const uint64_t i = g * 32 + lane;
+    const uint32_t kmask = (1u << kshift) - 1u;
+
+    // ---- the Sparse Table part (lane-private), as ml_one
+    uint32_t l = 0, r = 0;
+    bool s0 = false, s1 = false;  // sides: [l, min(r, end of l's block)], [start of r's block, r]
+    uint64_t best = kNoKey;
+    bool write = false;
+    if (i < q) {
+        // queries, answers and the rows are streamed (evict-first): the Sparse
+        // Table and the sub-block keys stay in L2 (measured: -7% on c3)
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(Q) + i);
+        uint64_t a = x.x, b = x.y;
+        if (a > b) { const uint64_t t = a; a = b; b = t; }  // types.hpp:18-20
+        if (b >= n) {                                        // naive.hpp:14-15
+            atomicOr(err, 1u);
+            answers[i] = ~0ull;
+        } else if (a == b) {
+            answers[i] = a;
+        } else {
+            write = true;
+            l = uint32_t(a);
+            r = uint32_t(b);
+            const uint32_t bl = l >> kshift, br = r >> kshift;
+            const uint64_t Lk = __ldg(ST + bl);
+            if (bl == br) {
+                if (key_pos(Lk) >= l && key_pos(Lk) <= r) best = Lk;
+                else s0 = true;
+            } else {
+                if (br - bl >= 2) {  // inner_span_min
+                    const uint32_t e = 31 - __clz(br - bl - 1);
+                    const uint64_t* row = ST + uint64_t(e) * stride;
+                    best = kmin(__ldg(row + bl + 1), __ldg(row + br - (1u << e)));
+                }
+                const uint64_t Rk = __ldg(ST + br);
+                if (best == kNoKey || key_hi(Rk) < key_hi(best)) {
+                    if (key_pos(Rk) <= r) best = kmin(best, Rk);
+                    else s1 = true;
+                }
+                if (best == kNoKey || key_hi(Lk) <= key_hi(best)) {
+                    if (key_pos(Lk) >= l) best = kmin(best, Lk);
+                    else s0 = true;
+                }
+            }
+        }
+    }
+
+    // ---- sides (lane-private, one fixed-shape pass per warp)
+    RowTask ra, rb;
+    if (__any_sync(kFull, s0 || s1)) {
+        RowTask r0l, r0r, r1l, r1r;
+        const uint64_t c0 = side_flat(sub, s0, l, min(r, l | kmask), kshift - 5, r0l, r0r);
+        const uint64_t c1 = side_flat(sub, s1, r & ~kmask, r, kshift - 5, r1l, r1r);
+        best = kmin(best, kmin(c0, c1));
+        // side 1 starts on a sub-block boundary: one row at most (its left row when
+        // it ends in its first sub-block, else its right row); side 0 has a right
+        // row only inside one block, where there is no side 1: <= 2 rows per lane
+        ra = r0l;
+        rb = r0r.need ? r0r : r1l.need ? r1l : r1r;
+    } else {
+        ra.need = rb.need = false;
+    }
+
+    // ---- rows: pooled per warp, half-warp scans
+    ra.need = ra.need && ((uint64_t(ra.v) << 32 | ra.lo) < best);
+    rb.need = rb.need && ((uint64_t(rb.v) << 32 | rb.lo) < best);
+    const unsigned ma = __ballot_sync(kFull, ra.need), mb = __ballot_sync(kFull, rb.need);
+    if (ma | mb) {
+        const unsigned below = (1u << lane) - 1u;
+        if (ra.need) s_rows[__popc(ma & below)] = make_uint4(ra.lo, ra.hi, ra.v, lane);
+        if (rb.need) s_rows[__popc(ma) + __popc(mb & below)] = make_uint4(rb.lo, rb.hi, rb.v, lane);
+        __syncwarp();
+        const uint32_t nrows = __popc(ma) + __popc(mb);
+        for (uint32_t e0 = 0; e0 < nrows; e0 += 2 * kMlBatch) {
+            uint64_t key[kMlBatch];
+            uint32_t own[kMlBatch];
+#pragma unroll
+            for (int u = 0; u < kMlBatch; ++u) {
+                const uint32_t e = e0 + 2 * u + (upper ? 1u : 0u);
+                const uint4 t = e < nrows ? s_rows[e] : make_uint4(1, 0, 0, 0);  // lo > hi: empty
+                own[u] = t.w;
+                key[u] = kNoKey;
+                const uint64_t p = (uint64_t(t.x) & ~31ull) + 2 * j;
+                if (t.x <= t.y) {
+                    int32_t v0, v1;
+                    if (VEC && p + 1 < n) {
+                        const int2 v = __ldcs(reinterpret_cast<const int2*>(A + p));
+                        v0 = v.x;
+                        v1 = v.y;
+                    } else {
+                        v0 = p < n ? __ldg(A + p) : 0;
+                        v1 = p + 1 < n ? __ldg(A + p + 1) : 0;
+                    }
+                    if (p >= t.x && p <= t.y) key[u] = pack_key(v0, uint32_t(p));
+                    if (p + 1 >= t.x && p + 1 <= t.y) key[u] = kmin(key[u], pack_key(v1, uint32_t(p + 1)));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kMlBatch; ++u) {
+                if (e0 + 2 * u >= nrows) break;  // warp-uniform
+                const uint64_t cand = half_min_key(key[u], upper);
+                const uint64_t c0 = shfl_u64(cand, 0), c1 = shfl_u64(cand, 16);
+                const uint32_t o0 = __shfl_sync(kFull, own[u], 0), o1 = __shfl_sync(kFull, own[u], 16);
+                if (lane == o0) best = kmin(best, c0);
+                if (e0 + 2 * u + 1 < nrows && lane == o1) best = kmin(best, c1);
+            }
+        }
+    }
+    if (write) __stcs(reinterpret_cast<unsigned long long*>(answers + i), (unsigned long long)key_pos(best));
+    __syncwarp();  // the row pool is reused by the warp's next group
+}
+
+template <bool VEC, int NT>
+__global__ void __launch_bounds__(NT) k_query_ml_flat(
+    const int32_t* __restrict__ A, uint64_t n, uint32_t kshift, const uint64_t* __restrict__ ST,
+    uint64_t stride, const uint64_t* __restrict__ sub, const uint64_t* __restrict__ Q, uint64_t q,
+    uint64_t* __restrict__ answers, uint32_t* __restrict__ err, const CtlPublish pub) {
+    constexpr int kRowCap = 64;  // <= 2 rows per lane
+    __shared__ uint4 s_rows[NT / 32][kRowCap];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t g = uint64_t(blockIdx.x) * (NT / 32) + warp;
+    if (g < (q + 31) / 32)
+        ml_flat_group<VEC>(A, n, kshift, ST, stride, sub, Q, q, answers, err, g, s_rows[warp]);
+    publish_control(pub);
+}
+
 }  // namespace
 
 int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
@@ -504,6 +713,16 @@ int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST
                     uint32_t* err, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
     const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
+    if (k >= 64 && k <= 512 && (k & (k - 1)) == 0) {
+        const bool vec = (reinterpret_cast<uintptr_t>(A) & 7u) == 0;
+        const uint32_t ks = floor_log2_u64(k);  // power-of-two k, <= 16 sub-blocks per block
+        // 128-thread CTAs: a CTA holds its slot until its slowest warp is done
+        // (measured vs 64 / 256: best over c3, c4 and c5)
+        const unsigned g = unsigned((q + 127) / 128);
+        if (vec) k_query_ml_flat<true, 128><<<g, 128, 0, stream>>>(A, n, ks, ST, b, sub, Q, q, answers, err, pub);
+        else k_query_ml_flat<false, 128><<<g, 128, 0, stream>>>(A, n, ks, ST, b, sub, Q, q, answers, err, pub);
+        return 1;
+    }
     if ((reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
     else

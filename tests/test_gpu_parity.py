@@ -129,8 +129,25 @@ def test_multilevel_configs(engine, orc):
     A = _values(r, 70_001, "ties16")
     Q = _queries(r, 70_001, 20_000, "mixed")
     want = orc.naive_numpy(A, Q)
-    for ks in [(512,), (32, 64), (32, 96), (32, 512), (32, 4096)]:
+    for ks in [(512,), (32, 64), (32, 96), (32, 128), (32, 512), (32, 1024), (32, 4096)]:
         assert np.array_equal(engine.solve_batch_bbst_ml(A, Q, ks), want), ks
+    # short ranges over sorted runs with ties: most queries descend to rows
+    A2 = np.sort(_values(r, 70_010, "ties16").reshape(10, 7001), axis=1)
+    A2[1::2] = A2[1::2, ::-1]  # ascending and descending runs
+    A2 = np.ascontiguousarray(A2).ravel()
+    for kind in ("short", "uniform"):
+        Q2 = _queries(r, A2.shape[0], 20_000, kind)
+        want2 = orc.naive_numpy(A2, Q2)
+        for ks in [(32, 64), (32, 512)]:
+            assert np.array_equal(engine.solve_batch_bbst_ml(A2, Q2, ks), want2), (kind, ks)
+    # short ranges straddling a block boundary: both sides descend, each to one
+    # partial row (the right side's row lies in its first sub-block)
+    A3 = _values(r, 50_000, "uniform")
+    for k in (64, 128, 256, 512):
+        edge = (r.integers(1, 50_000 // k, 5000) * k).astype(np.int64)
+        Q3 = np.stack([edge - r.integers(1, 40, 5000), edge + r.integers(0, 40, 5000)], 1)
+        Q3 = np.clip(Q3, 0, 49_999).astype(np.uint64)
+        assert np.array_equal(engine.solve_batch_bbst_ml(A3, Q3, (32, k)), orc.naive_numpy(A3, Q3)), k
     for bad in [(16, 512), (32, 48), (32, 16), (64, 512), (32, 64, 512)]:
         with pytest.raises(InvalidArgument):
             engine.solve_batch_bbst_ml(A, Q, bad)

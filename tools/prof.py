@@ -20,6 +20,8 @@ dQ = torch.from_numpy(Q.view(np.int64)).cuda()
 for _ in range(a.iters):
     if a.variant == 'bbst':
         out = eng.solve_batch_bbst(dA, dQ, 512)
+    elif a.variant == 'bbst_ml':
+        out = eng.solve_batch_bbst_ml(dA, dQ, (32, 512))
     else:
         out = eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[a.variant])
 torch.cuda.synchronize()
