@@ -56,7 +56,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 struct Control {
     uint32_t err;       // 1 query out of range (direct), 2 range (collect/unique), 4 unsorted, 8 logic
     uint32_t span[2];   // [~min endpoint, max endpoint]
-    uint32_t tickets[5];
+    uint32_t tickets[5];  // last-CTA tickets: [0] k_unique, [4] publish
     uint64_t nb;        // |boundary|
     uint64_t aq_len;    // |A_Q|
     uint64_t b_dev;     // blocks over A_Q
