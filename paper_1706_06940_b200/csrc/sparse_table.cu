@@ -12,7 +12,8 @@
 // doubles D times in shared memory (ping-pong buffers, one barrier per level)
 // and writes each finished level straight to its row.  base = 0 uses R = 1
 // (plain contiguous columns, D <= 10, T = 2048); higher bases use R = 16
-// residues (128-byte runs, D <= 7, T = 64).  The loops are split so that the
+// residues (128-byte runs, D <= 7, T = 128), and the last launch of a large
+// table, which has at most 32 t-positions, trades them for 32 or 64 residues.  The loops are split so that the
 // store predicate is a single 32-bit compare against a per-level limit.
 // b = 2M (n = 2^30, k = 512, 22 levels) needs 3 launches instead of 21.
 #include "common.cuh"
@@ -99,7 +100,16 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
             base = D;
         } else {
             const uint32_t D = (L - 1 - base) < 7 ? (L - 1 - base) : 7;
-            launches += launch_tile<16, 64, 256>(ST, b, b_dev, base, D, stream);  // base >= 10
+            // base >= 10.  The last launch of a table has few t-positions
+            // (tcount = b >> base, 2^D of them at most): trade t for residues so
+            // its CTAs are not mostly empty windows
+            const uint64_t tcount = (b + (1ull << base) - 1) >> base;
+            if (tcount <= 16)
+                launches += launch_tile<64, 16, 256>(ST, b, b_dev, base, D, stream);
+            else if (tcount <= 32)
+                launches += launch_tile<32, 32, 256>(ST, b, b_dev, base, D, stream);
+            else  // (measured: T = 128 x 512 threads beats 64 x 256 and 256 x 512)
+                launches += launch_tile<16, 128, 512>(ST, b, b_dev, base, D, stream);
             base += D;
         }
     }

@@ -264,7 +264,8 @@ def test_stage_contract_errors(engine):
 def test_stage_block_sparse(engine, orc, k):
     import ctypes as C
     r = np.random.default_rng(k)
-    for m in (1, 2, 5, 1000, 100_000):
+    # k <= 2 at 2^21 + 777 keys: 22 levels, all three tiled launches (bases 0, 10, 17)
+    for m in (1, 2, 5, 1000, 100_000) + (((1 << 21) + 777,) if k <= 2 else ()):
         v = _values(r, m, "ties16")
         table, b, levels = engine.build_block_sparse(v, k)
         ref = np.empty(max(levels * b, 1), np.uint64)
