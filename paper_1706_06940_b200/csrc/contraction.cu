@@ -171,6 +171,48 @@ __device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, 
     run = ri >= 0 ? pack_key(rv, uint32_t(rw.pos(r, ri))) : kNoKey;
 }
 
+// row_pass for an interior row (all 32 positions in the span), run by EVERY lane
+// of a dense tile: a row without boundaries comes out with its minimum in
+// `run`, so the unflagged lanes do their row minimum in the same instruction
+// stream instead of a separate, serialised row_min pass; element 0 is peeled
+// (the run is never empty after it).
+template <bool MARKED, class RW>
+__device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t fl, uint64_t rank,
+                                             uint64_t* __restrict__ aq, uint64_t& hp,
+                                             uint64_t& run) {
+    const uint32_t p0 = uint32_t(rw.pos(r, 0));
+    int4 x = rw.chunk(r, 0);
+    int32_t rv = x.x;
+    uint32_t ri = 0;
+    bool seen = fl & 1u;
+    if (seen) hp = pack_key(rv, p0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if (c) x = rw.chunk(r, c);
+#pragma unroll
+        for (int e = (c == 0 ? 1 : 0); e < 4; ++e) {
+            const int j = 4 * c + e;
+            const int32_t v = comp(x, e);
+            if ((fl >> j) & 1u) {
+                const uint64_t k = v < rv ? pack_key(v, p0 + j) : pack_key(rv, p0 + ri);
+                if (seen) {
+                    aq[aq_slot<MARKED>(rank)] = k;
+                    ++rank;
+                } else {
+                    hp = k;
+                    seen = true;
+                }
+                rv = v;  // the boundary element opens the next area
+                ri = j;
+            } else if (v < rv) {
+                rv = v;
+                ri = j;
+            }
+        }
+    }
+    run = pack_key(rv, p0 + ri);
+}
+
 // Warp `warp`'s piece of CTA `cta`'s range: warp tiles [wa, wa + cnt) of range
 // cta (R tiles), clipped to the span [b0, blast]; cnt = 0 when empty.  Shared by
 // the contraction and the piece-count kernel, so both cut identically.
@@ -407,7 +449,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
         // pass 1: open-segment key at the right end of the lane's row; a dense
         // tile's flagged rows are handled in one pass below instead
         uint64_t run = kNoKey;
-        if (any && fl == 0)
+        if (any && fl == 0 && (GEN || !dense))  // (dense interior tiles: row_pass_all below)
             run = !GEN ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, jlo, jhi);
         uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (!dense) {  // sparse flagged rows: one element per lane
@@ -445,7 +487,8 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             wc = __shfl_sync(kFull, cinc, 31);
             const uint64_t rank = rank_run + (cinc - cntb);
             uint64_t hp = kNoKey;
-            if (any && fl) row_pass<MARKED>(rs, lane, fl, jlo, jhi, rank, c.aq, hp, run);
+            if (!GEN) row_pass_all<MARKED>(rs, lane, fl, rank, c.aq, hp, run);
+            else if (any && fl) row_pass<MARKED>(rs, lane, fl, jlo, jhi, rank, c.aq, hp, run);
             SegMin inc{run, cntb != 0};
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
