@@ -822,6 +822,10 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const size_t i_cr = cv.add(q * 4);
     const size_t i_aq = cv.add((aq_max + 2) * 8);
     const size_t i_st = cv.add(size_t(L) * b_max * 8);
+    // power-of-two k in [64, 512]: 32-key sub-block minima over A_Q as a second level
+    // (answers identical; partial blocks are resolved through them, DESIGN 3.2)
+    const bool sub_level = k >= 64 && k <= 512 && (k & (k - 1)) == 0;
+    const size_t i_sub = cv.add(sub_level ? ((aq_max + 31) / 32 + 2) * 8 : 0);
     Carve sv;  // status arena
     const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
     const size_t i_pc = cv.add(size_t(brmq::kMaxContractRanges) * brmq::kContractWarps * 4);
@@ -907,8 +911,11 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         launches += l;
         tm.end(l);
         // (bitmap pipeline: the query remap is folded into the query kernel)
+        auto* SUB = reinterpret_cast<uint64_t*>(P(i_sub));
         tm.stage("block_argmin", launches);
-        l = brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
+        l = sub_level ? brmq::launch_block_argmin_keys_ml(AQ, aq_max, &ctl->aq_len, k, ST, SUB,
+                                                          &ctl->b_dev, s)
+                      : brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
         launches += l;
         tm.end(l);
         tm.stage("sparse_table", launches);
@@ -916,11 +923,15 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = use_bitmap ? brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ,
-                                                          reinterpret_cast<uint2*>(P(i_wi)), n, q,
-                                                          dAns, s, publish(c, ctl))
-                       : brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl, cr,
-                                                       q, dAns, s, publish(c, ctl));
+        const uint2* wi = use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr;
+        if (sub_level)
+            l = brmq::launch_query_con_flat(AQ, k, ST, b_max, SUB, dQ, wi, cl, cr, n, q, dAns, s,
+                                            publish(c, ctl));
+        else
+            l = use_bitmap ? brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ, wi, n, q, dAns, s,
+                                                              publish(c, ctl))
+                           : brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl,
+                                                           cr, q, dAns, s, publish(c, ctl));
         launches += l;
         tm.end(l);
         if (int rc = check_status(c)) return rc;

@@ -233,6 +233,47 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_ml_gen(const int32_t*
     if (lane == 0) keys[blk] = best;
 }
 
+// Two-level minima over packed keys (A_Q of BbST_CON, device-side length): the
+// k-block keys and the 32-key sub-block keys in one pass.  k a multiple of 64,
+// A_Q 16-byte aligned and padded to an even count: lane l of round u holds keys
+// 2(32u + l) and 2(32u + l) + 1 of the block, so a half warp covers one
+// sub-block.
+__global__ void __launch_bounds__(kThreads) k_block_argmin_keys_ml(
+    const uint64_t* __restrict__ K, const uint64_t* __restrict__ len_dev, uint64_t len_max,
+    uint32_t k, uint64_t* __restrict__ keys, uint64_t* __restrict__ sub,
+    uint64_t* __restrict__ b_dev) {
+    const uint64_t len = len_dev ? *len_dev : len_max;
+    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
+    const uint64_t lo = blk * k;
+    if (lo >= len) return;
+    const unsigned lane = lane_id();
+    const uint4* v4 = reinterpret_cast<const uint4*>(K + lo);
+    const uint32_t nvec = k >> 1;  // multiple of 32
+    uint64_t best = kNoKey;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
+        uint4 x[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t e = lo + 2 * uint64_t(v0 + 32 * u + lane);
+            x[u] = v0 + 32 * u < nvec && e < len ? ld_stream_u4(v4 + v0 + 32 * u + lane)
+                                                 : make_uint4(~0u, ~0u, ~0u, ~0u);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (v0 + 32 * u >= nvec) break;
+            const uint64_t e = lo + 2 * uint64_t(v0 + 32 * u + lane);
+            uint64_t kk = (uint64_t(x[u].y) << 32) | x[u].x;
+            if (e + 1 < len) kk = kmin(kk, (uint64_t(x[u].w) << 32) | x[u].z);
+            kk = group_min_key<16>(kk);  // the half warp's sub-block
+            if ((lane & 15u) == 0 && e < len) sub[e >> 5] = kk;
+            best = kmin(best, kk);
+        }
+    }
+    best = warp_min_key(best);
+    if (lane == 0) keys[blk] = best;
+}
+
 }  // namespace
 
 int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
@@ -244,6 +285,16 @@ int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* k
                                                                             sub);
     else
         k_block_argmin_ml_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, nblk, k, keys, sub);
+    return 1;
+}
+
+int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
+                                uint32_t k, uint64_t* keys, uint64_t* sub, uint64_t* b_dev,
+                                cudaStream_t stream) {
+    uint64_t nblk = (len_max + k - 1) / k;
+    if (nblk == 0) nblk = 1;  // still publish *b_dev
+    k_block_argmin_keys_ml<<<grid_for_warps(nblk), kThreads, 0, stream>>>(K, len_dev, len_max, k,
+                                                                          keys, sub, b_dev);
     return 1;
 }
 

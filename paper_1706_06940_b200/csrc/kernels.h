@@ -32,6 +32,11 @@ int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t
 
 // Multi-level (k1 = 32) variant: also stores the leftmost-min key of every
 // 32-element sub-block in sub[ceil(n/32)] (k must be a multiple of 32).
+// A_Q keys: k-block keys + 32-key sub-block keys (k a multiple of 64, A_Q padded
+// to an even count, 16-byte aligned), device-side length.
+int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
+                                uint32_t k, uint64_t* keys, uint64_t* sub, uint64_t* b_dev,
+                                cudaStream_t stream);
 int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
                            uint64_t* sub, cudaStream_t stream);
 
@@ -55,6 +60,12 @@ int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST
                     uint32_t* err, cudaStream_t stream,
                     const CtlPublish& pub = CtlPublish{});
 // bitmap pipeline: contracted coordinates from the contraction's word_info
+// BbST_CON answering with the sub-block level over A_Q (k a power of two in
+// [64, 512]; launch_block_argmin_keys_ml built ST level 0 and `sub`).
+int launch_query_con_flat(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
+                          const uint64_t* sub, const uint64_t* Q, const uint2* word_info,
+                          const uint32_t* cleft, const uint32_t* cright_raw, uint64_t n, uint64_t q,
+                          uint64_t* answers, cudaStream_t stream, const CtlPublish& pub);
 int launch_query_contracted_wi(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
                                const uint64_t* Q, const uint2* word_info, uint64_t n, uint64_t q,
                                uint64_t* answers, cudaStream_t stream,

@@ -530,19 +530,59 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
     return (uint64_t(b) << 32) | a;
 }
 
-// One partial edge row: A[lo..hi] inside one 32-aligned row, scanned only if
-// pack(v, lo) (v = the stored minimum of its sub-block, which lies outside the
-// row part) is below the owner's best.
+// One partial edge row: elements [lo..hi] of one 32-aligned row, scanned only
+// if pack(v, a) -- v the stored minimum of its sub-block, which lies outside the
+// row part, a a lower bound on the positions in the row part -- is below the
+// owner's best.
 struct RowTask {
-    uint32_t lo, hi, v;
+    uint32_t lo, hi, v, a;
     bool need;
 };
 
-// Side [lo, hi] (act: this lane has the side) against the block's sub-block
-// keys: the minimum over the covered sub-blocks whose key lies inside, and the
-// edge rows left to scan.  ks = log2(k / 32).
+// Row loaders: min key of elements p, p + 1 (p even) that lie in [lo, hi].
+template <bool VEC>
+struct RowI32 {  // A itself: positions are indices
+    const int32_t* A;
+    uint64_t n;
+    static constexpr bool kDirect = true;
+    __device__ __forceinline__ uint64_t pair(uint64_t p, uint32_t lo, uint32_t hi) const {
+        int32_t v0, v1;
+        if (VEC && p + 1 < n) {
+            const int2 v = __ldcs(reinterpret_cast<const int2*>(A + p));
+            v0 = v.x;
+            v1 = v.y;
+        } else {
+            v0 = p < n ? __ldg(A + p) : 0;
+            v1 = p + 1 < n ? __ldg(A + p + 1) : 0;
+        }
+        uint64_t k = kNoKey;
+        if (p >= lo && p <= hi) k = pack_key(v0, uint32_t(p));
+        if (p + 1 >= lo && p + 1 <= hi) k = kmin(k, pack_key(v1, uint32_t(p + 1)));
+        return k;
+    }
+};
+struct RowKey {  // A_Q: packed keys carrying original positions (16-byte aligned, even-padded)
+    const uint64_t* K;
+    static constexpr bool kDirect = false;
+    __device__ __forceinline__ uint64_t pair(uint64_t p, uint32_t lo, uint32_t hi) const {
+        if (p > hi || p + 1 < lo) return kNoKey;  // never reads past the row part
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(K + p));
+        uint64_t k = p >= lo ? (uint64_t(v.y) << 32) | v.x : kNoKey;
+        if (p + 1 <= hi) k = kmin(k, (uint64_t(v.w) << 32) | v.z);
+        return k;
+    }
+};
+
+// Side [lo, hi] of element indices inside one k-block (act: this lane has the
+// side) against the block's sub-block keys: the minimum over the covered
+// sub-blocks whose key lies inside, and the edge rows left to scan.  The
+// "inside" tests are on original positions [plo, phi] (for A_Q exact because
+// the origins are non-decreasing: a key at the bound is also the key of an
+// index inside, SPEC.md:231 / DESIGN 3.2).  ks = log2(k / 32).
+template <bool DIRECT>
 __device__ __forceinline__ uint64_t side_flat(const uint64_t* __restrict__ sub, bool act, uint32_t lo,
-                                              uint32_t hi, uint32_t ks, RowTask& rl, RowTask& rr) {
+                                              uint32_t hi, uint32_t plo, uint32_t phi, uint32_t ks,
+                                              RowTask& rl, RowTask& rr) {
     const uint32_t sl = lo >> 5, sr = hi >> 5, sb = (sl >> ks) << ks, K = 1u << ks;
     const ulonglong2* sub2 = reinterpret_cast<const ulonglong2*>(sub + sb);
     ulonglong2 x[8];
@@ -561,52 +601,53 @@ __device__ __forceinline__ uint64_t side_flat(const uint64_t* __restrict__ sub, 
     }
     rl.need = rr.need = false;
     if (act) {
-        if (key_pos(kl) >= lo && key_pos(kl) <= hi) cand = kmin(cand, kl);
-        else rl = RowTask{lo, sl == sr ? hi : (sl << 5) + 31, key_hi(kl), true};
+        if (key_pos(kl) >= plo && key_pos(kl) <= phi) cand = kmin(cand, kl);
+        else rl = RowTask{lo, sl == sr ? hi : (sl << 5) + 31, key_hi(kl), DIRECT ? lo : plo, true};
         if (sr != sl) {
-            if (key_pos(kr) <= hi) cand = kmin(cand, kr);
-            else rr = RowTask{sr << 5, hi, key_hi(kr), true};
+            if (key_pos(kr) <= phi) cand = kmin(cand, kr);
+            else rr = RowTask{sr << 5, hi, key_hi(kr), DIRECT ? (sr << 5) : plo, true};
         }
     }
     return cand;
 }
 
-// One warp answers queries [g * 32, g * 32 + 32) (lane = query).
-template <bool VEC>
-__device__ __forceinline__ void ml_flat_group(
-    const int32_t* __restrict__ A, uint64_t n, uint32_t kshift, const uint64_t* __restrict__ ST,
-    uint64_t stride, const uint64_t* __restrict__ sub, const uint64_t* __restrict__ Q, uint64_t q,
-    uint64_t* __restrict__ answers, uint32_t* __restrict__ err, uint64_t g, uint4* s_rows) {
+// One warp answers queries [g * 32, g * 32 + 32) (lane = query).  E: row loader
+// of the scanned array (A, or A_Q), QP: query resolution (direct, or the
+// contracted coordinates of BbST_CON).
+template <class E, class QP>
+__device__ __forceinline__ void ml_flat_group(const E& elem, const QP& qp, uint32_t kshift,
+                                              const uint64_t* __restrict__ ST, uint64_t stride,
+                                              const uint64_t* __restrict__ sub, uint64_t q,
+                                              uint64_t* __restrict__ answers, uint64_t g,
+                                              uint4* s_rows) {
     const uint32_t lane = lane_id();
     const bool upper = lane >= 16;
     const uint32_t j = lane & 15u;
     const uint64_t i = g * 32 + lane;
     const uint32_t kmask = (1u << kshift) - 1u;
 
-    // ---- the Sparse Table part (lane-private), as ml_one
-    uint32_t l = 0, r = 0;
-    bool s0 = false, s1 = false;  // sides: [l, min(r, end of l's block)], [start of r's block, r]
+    // ---- the Sparse Table part (lane-private), as ml_one / answer_one
+    uint32_t il = 0, ir = 0, pl = 0, pr = 0;
+    bool s0 = false, s1 = false, inblk = false;  // sides: [il, min(ir, end of il's block)], [start of ir's block, ir]
     uint64_t best = kNoKey;
     bool write = false;
     if (i < q) {
         // queries, answers and the rows are streamed (evict-first): the Sparse
         // Table and the sub-block keys stay in L2 (measured: -7% on c3)
-        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(Q) + i);
-        uint64_t a = x.x, b = x.y;
-        if (a > b) { const uint64_t t = a; a = b; b = t; }  // types.hpp:18-20
-        if (b >= n) {                                        // naive.hpp:14-15
-            atomicOr(err, 1u);
-            answers[i] = ~0ull;
-        } else if (a == b) {
-            answers[i] = a;
+        const Resolved rq = qp.resolve(i);
+        if (rq.done) {
+            __stcs(reinterpret_cast<unsigned long long*>(answers + i), (unsigned long long)rq.direct);
         } else {
             write = true;
-            l = uint32_t(a);
-            r = uint32_t(b);
-            const uint32_t bl = l >> kshift, br = r >> kshift;
+            il = uint32_t(rq.il);
+            ir = uint32_t(rq.ir);
+            pl = uint32_t(rq.pl);
+            pr = uint32_t(rq.pr);
+            const uint32_t bl = il >> kshift, br = ir >> kshift;
             const uint64_t Lk = __ldg(ST + bl);
             if (bl == br) {
-                if (key_pos(Lk) >= l && key_pos(Lk) <= r) best = Lk;
+                inblk = true;
+                if (key_pos(Lk) >= pl && key_pos(Lk) <= pr) best = Lk;
                 else s0 = true;
             } else {
                 if (br - bl >= 2) {  // inner_span_min
@@ -616,11 +657,11 @@ __device__ __forceinline__ void ml_flat_group(
                 }
                 const uint64_t Rk = __ldg(ST + br);
                 if (best == kNoKey || key_hi(Rk) < key_hi(best)) {
-                    if (key_pos(Rk) <= r) best = kmin(best, Rk);
+                    if (key_pos(Rk) <= pr) best = kmin(best, Rk);
                     else s1 = true;
                 }
                 if (best == kNoKey || key_hi(Lk) <= key_hi(best)) {
-                    if (key_pos(Lk) >= l) best = kmin(best, Lk);
+                    if (key_pos(Lk) >= pl) best = kmin(best, Lk);
                     else s0 = true;
                 }
             }
@@ -631,8 +672,9 @@ __device__ __forceinline__ void ml_flat_group(
     RowTask ra, rb;
     if (__any_sync(kFull, s0 || s1)) {
         RowTask r0l, r0r, r1l, r1r;
-        const uint64_t c0 = side_flat(sub, s0, l, min(r, l | kmask), kshift - 5, r0l, r0r);
-        const uint64_t c1 = side_flat(sub, s1, r & ~kmask, r, kshift - 5, r1l, r1r);
+        const uint64_t c0 = side_flat<E::kDirect>(sub, s0, il, min(ir, il | kmask), pl,
+                                                  inblk ? pr : 0xFFFFFFFFu, kshift - 5, r0l, r0r);
+        const uint64_t c1 = side_flat<E::kDirect>(sub, s1, ir & ~kmask, ir, 0u, pr, kshift - 5, r1l, r1r);
         best = kmin(best, kmin(c0, c1));
         // side 1 starts on a sub-block boundary: one row at most (its left row when
         // it ends in its first sub-block, else its right row); side 0 has a right
@@ -644,13 +686,15 @@ __device__ __forceinline__ void ml_flat_group(
     }
 
     // ---- rows: pooled per warp, half-warp scans
-    ra.need = ra.need && ((uint64_t(ra.v) << 32 | ra.lo) < best);
-    rb.need = rb.need && ((uint64_t(rb.v) << 32 | rb.lo) < best);
+    ra.need = ra.need && ((uint64_t(ra.v) << 32 | ra.a) < best);
+    rb.need = rb.need && ((uint64_t(rb.v) << 32 | rb.a) < best);
     const unsigned ma = __ballot_sync(kFull, ra.need), mb = __ballot_sync(kFull, rb.need);
     if (ma | mb) {
+        // entry: lo, (hi - lo) | owner << 8, (the bound needs no re-check: best only falls)
         const unsigned below = (1u << lane) - 1u;
-        if (ra.need) s_rows[__popc(ma & below)] = make_uint4(ra.lo, ra.hi, ra.v, lane);
-        if (rb.need) s_rows[__popc(ma) + __popc(mb & below)] = make_uint4(rb.lo, rb.hi, rb.v, lane);
+        if (ra.need) s_rows[__popc(ma & below)] = make_uint4(ra.lo, (ra.hi - ra.lo) | (lane << 8), 0, 0);
+        if (rb.need)
+            s_rows[__popc(ma) + __popc(mb & below)] = make_uint4(rb.lo, (rb.hi - rb.lo) | (lane << 8), 0, 0);
         __syncwarp();
         const uint32_t nrows = __popc(ma) + __popc(mb);
         for (uint32_t e0 = 0; e0 < nrows; e0 += 2 * kMlBatch) {
@@ -659,23 +703,10 @@ __device__ __forceinline__ void ml_flat_group(
 #pragma unroll
             for (int u = 0; u < kMlBatch; ++u) {
                 const uint32_t e = e0 + 2 * u + (upper ? 1u : 0u);
-                const uint4 t = e < nrows ? s_rows[e] : make_uint4(1, 0, 0, 0);  // lo > hi: empty
-                own[u] = t.w;
-                key[u] = kNoKey;
-                const uint64_t p = (uint64_t(t.x) & ~31ull) + 2 * j;
-                if (t.x <= t.y) {
-                    int32_t v0, v1;
-                    if (VEC && p + 1 < n) {
-                        const int2 v = __ldcs(reinterpret_cast<const int2*>(A + p));
-                        v0 = v.x;
-                        v1 = v.y;
-                    } else {
-                        v0 = p < n ? __ldg(A + p) : 0;
-                        v1 = p + 1 < n ? __ldg(A + p + 1) : 0;
-                    }
-                    if (p >= t.x && p <= t.y) key[u] = pack_key(v0, uint32_t(p));
-                    if (p + 1 >= t.x && p + 1 <= t.y) key[u] = kmin(key[u], pack_key(v1, uint32_t(p + 1)));
-                }
+                const uint4 t = e < nrows ? s_rows[e] : make_uint4(0, 0, 0, 0);
+                own[u] = t.y >> 8;
+                key[u] = e < nrows ? elem.pair((uint64_t(t.x) & ~31ull) + 2 * j, t.x, t.x + (t.y & 31u))
+                                   : kNoKey;
             }
 #pragma unroll
             for (int u = 0; u < kMlBatch; ++u) {
@@ -692,18 +723,31 @@ __device__ __forceinline__ void ml_flat_group(
     __syncwarp();  // the row pool is reused by the warp's next group
 }
 
-template <bool VEC, int NT>
-__global__ void __launch_bounds__(NT) k_query_ml_flat(
-    const int32_t* __restrict__ A, uint64_t n, uint32_t kshift, const uint64_t* __restrict__ ST,
-    uint64_t stride, const uint64_t* __restrict__ sub, const uint64_t* __restrict__ Q, uint64_t q,
-    uint64_t* __restrict__ answers, uint32_t* __restrict__ err, const CtlPublish pub) {
+template <class E, class QP, int NT>
+__global__ void __launch_bounds__(NT) k_query_flat(const E elem, const QP qp, uint32_t kshift,
+                                                   const uint64_t* __restrict__ ST, uint64_t stride,
+                                                   const uint64_t* __restrict__ sub, uint64_t q,
+                                                   uint64_t* __restrict__ answers,
+                                                   const CtlPublish pub) {
     constexpr int kRowCap = 64;  // <= 2 rows per lane
     __shared__ uint4 s_rows[NT / 32][kRowCap];
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t g = uint64_t(blockIdx.x) * (NT / 32) + warp;
-    if (g < (q + 31) / 32)
-        ml_flat_group<VEC>(A, n, kshift, ST, stride, sub, Q, q, answers, err, g, s_rows[warp]);
+    if (g < (q + 31) / 32) ml_flat_group(elem, qp, kshift, ST, stride, sub, q, answers, g, s_rows[warp]);
     publish_control(pub);
+}
+
+// 128-thread CTAs: a CTA holds its slot until its slowest warp is done
+// (measured vs 64 / 256: best over c3, c4 and c5)
+constexpr int kFlatThreads = 128;
+
+template <class E, class QP>
+void launch_flat(const E& e, const QP& qp, uint32_t k, const uint64_t* ST, uint64_t stride,
+                 const uint64_t* sub, uint64_t q, uint64_t* answers, cudaStream_t s,
+                 const CtlPublish& pub) {
+    const unsigned g = unsigned((q + kFlatThreads - 1) / kFlatThreads);
+    k_query_flat<E, QP, kFlatThreads><<<g, kFlatThreads, 0, s>>>(e, qp, floor_log2_u64(k), ST, stride,
+                                                                  sub, q, answers, pub);
 }
 
 }  // namespace
@@ -713,20 +757,35 @@ int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST
                     uint32_t* err, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
     const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
-    if (k >= 64 && k <= 512 && (k & (k - 1)) == 0) {
-        const bool vec = (reinterpret_cast<uintptr_t>(A) & 7u) == 0;
-        const uint32_t ks = floor_log2_u64(k);  // power-of-two k, <= 16 sub-blocks per block
-        // 128-thread CTAs: a CTA holds its slot until its slowest warp is done
-        // (measured vs 64 / 256: best over c3, c4 and c5)
-        const unsigned g = unsigned((q + 127) / 128);
-        if (vec) k_query_ml_flat<true, 128><<<g, 128, 0, stream>>>(A, n, ks, ST, b, sub, Q, q, answers, err, pub);
-        else k_query_ml_flat<false, 128><<<g, 128, 0, stream>>>(A, n, ks, ST, b, sub, Q, q, answers, err, pub);
+    if (k >= 64 && k <= 512 && (k & (k - 1)) == 0) {  // <= 16 sub-blocks per block
+        if ((reinterpret_cast<uintptr_t>(A) & 7u) == 0)
+            launch_flat(RowI32<true>{A, n}, QueryDirect{Q, n, err}, k, ST, b, sub, q, answers, stream, pub);
+        else
+            launch_flat(RowI32<false>{A, n}, QueryDirect{Q, n, err}, k, ST, b, sub, q, answers, stream, pub);
         return 1;
     }
     if ((reinterpret_cast<uintptr_t>(A) & 15u) == 0)
         k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
     else
         k_query_ml<false><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
+    return 1;
+}
+
+// BbST_CON with a sub-block level over A_Q (power-of-two k in [64, 512]): the
+// same flat answering as the multi-level BbST, over packed keys, from the
+// contracted coordinates.  wi != nullptr: bitmap pipeline (coordinates from the
+// per-word ranks), else cleft / cright_raw (radix pipeline).
+int launch_query_con_flat(const uint64_t* AQ, uint32_t k, const uint64_t* ST, uint64_t b_max,
+                          const uint64_t* sub, const uint64_t* Q, const uint2* word_info,
+                          const uint32_t* cleft, const uint32_t* cright_raw, uint64_t n, uint64_t q,
+                          uint64_t* answers, cudaStream_t stream, const CtlPublish& pub) {
+    if (q == 0) return 0;
+    if (word_info)
+        launch_flat(RowKey{AQ}, QueryContractedWI{Q, word_info, n}, k, ST, b_max, sub, q, answers,
+                    stream, pub);
+    else
+        launch_flat(RowKey{AQ}, QueryContracted{Q, cleft, cright_raw}, k, ST, b_max, sub, q, answers,
+                    stream, pub);
     return 1;
 }
 

@@ -148,6 +148,16 @@ def test_multilevel_configs(engine, orc):
         Q3 = np.stack([edge - r.integers(1, 40, 5000), edge + r.integers(0, 40, 5000)], 1)
         Q3 = np.clip(Q3, 0, 49_999).astype(np.uint64)
         assert np.array_equal(engine.solve_batch_bbst_ml(A3, Q3, (32, k)), orc.naive_numpy(A3, Q3)), k
+    # BbST_CON's sub-block level over A_Q (power-of-two k in [64, 512]): many short
+    # queries make A_Q long and the contracted ranges short -- sides and rows in
+    # A_Q index space, inside-tests on original positions (ties16: equal keys)
+    A4 = _values(r, 200_000, "ties16")
+    for kind in ("short", "mixed"):
+        Q4 = _queries(r, 200_000, 60_000, kind)
+        want4 = orc.naive_numpy(A4, Q4)
+        for k in (64, 256, 512):
+            for sk in (SortKind.Bitmap, SortKind.Radix):
+                assert np.array_equal(engine.solve_batch_bbst_con(A4, Q4, k, sk), want4), (kind, k, sk)
     for bad in [(16, 512), (32, 48), (32, 16), (64, 512), (32, 64, 512)]:
         with pytest.raises(InvalidArgument):
             engine.solve_batch_bbst_ml(A, Q, bad)
