@@ -122,6 +122,14 @@ int brmq_solve_bbst_shard(brmq_ctx* ctx, const int32_t* A, uint64_t n_shard, uin
                           uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
                           uint64_t* keys, uint32_t flags);
 
+/* Sharded BbST_CON (contraction variant): as brmq_solve_bbst_shard,
+ * with the shard solved by brmq_solve_bbst_con -- the shard is contracted with
+ * the endpoints that fall inside it plus the shard borders of the queries that
+ * cross them (the clipped queries' endpoints). */
+int brmq_solve_bbst_con_shard(brmq_ctx* ctx, const int32_t* A, uint64_t n_shard, uint64_t offset,
+                              uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
+                              int sort_kind, uint64_t* keys, uint32_t flags);
+
 /* naive.hpp:13-21 for every query, on the device (one warp per query): the
  * harness's "naive" algorithm. */
 int brmq_solve_naive(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,

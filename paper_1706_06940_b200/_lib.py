@@ -50,6 +50,8 @@ SIGNATURES = {
                                       C.c_uint32]),
     "brmq_solve_bbst_shard": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint64,
                                         C.c_uint32, vp, C.c_uint32]),
+    "brmq_solve_bbst_con_shard": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp,
+                                            C.c_uint64, C.c_uint32, C.c_int, vp, C.c_uint32]),
     "brmq_solve_naive": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, C.c_uint32]),
     "brmq_solve_st_rmq_con": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, C.c_uint32]),
     "brmq_collect_endpoints": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint32]),

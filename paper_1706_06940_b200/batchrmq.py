@@ -179,11 +179,7 @@ class Engine:
         """SPEC.md:237-245, BbST_CON (PAPER.md:210-272)."""
         return self._solve(True, array, batch, k, int(sort_kind), out)
 
-    def solve_batch_bbst_shard(self, shard, batch, offset: int, n_total: int, k: int = 512,
-                               out=None):
-        """Packed keys of every query restricted to A[offset, offset + len(shard)) with
-        global positions (UINT64_MAX when the query misses the shard); the min over
-        shards is the answer's key (include/brmq.h brmq_solve_bbst_shard)."""
+    def _shard(self, fn, shard, batch, offset, n_total, extra, out):
         if _is_cuda_tensor(shard):
             import torch
             ns, q = shard.numel(), batch.numel() // 2
@@ -197,9 +193,24 @@ class Engine:
             if out is None:
                 out = np.empty(q, dtype=np.uint64)
             a, b, o, flags = _ptr(shard), _ptr(batch), _ptr(out), PTR_HOST
-        _check(self._L.brmq_solve_bbst_shard(self._h, a, ns, int(offset), int(n_total), b, q,
-                                             int(k), o, flags))
+        _check(fn(self._h, a, ns, int(offset), int(n_total), b, q, *extra, o, flags))
         return out
+
+    def solve_batch_bbst_shard(self, shard, batch, offset: int, n_total: int, k: int = 512,
+                               out=None):
+        """Packed keys of every query restricted to A[offset, offset + len(shard)) with
+        global positions (UINT64_MAX when the query misses the shard); the min over
+        shards is the answer's key (include/brmq.h brmq_solve_bbst_shard)."""
+        return self._shard(self._L.brmq_solve_bbst_shard, shard, batch, offset, n_total,
+                           (int(k),), out)
+
+    def solve_batch_bbst_con_shard(self, shard, batch, offset: int, n_total: int, k: int = 512,
+                                   sort_kind: SortKind = SortKind.Radix, out=None):
+        """The contraction variant of solve_batch_bbst_shard: the shard is contracted with
+        its own endpoints plus the borders of the queries crossing it
+        (include/brmq.h brmq_solve_bbst_con_shard)."""
+        return self._shard(self._L.brmq_solve_bbst_con_shard, shard, batch, offset, n_total,
+                           (int(k), int(sort_kind)), out)
 
     def solve_batch_naive(self, array, batch, out=None):
         """naive.hpp:13-21 for every query (the harness's "naive"), on the device."""

@@ -508,11 +508,14 @@ __global__ void k_shard_keys(const uint64_t* __restrict__ loc, const uint8_t* __
     keys[i] = empty[i] ? ~0ull : brmq::pack_key(__ldg(A + p), uint32_t(off + p));
 }
 
-int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset,
-                          uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
-                          uint64_t* keys, uint32_t flags) {
-    if (!c) return fail(BRMQ_EINVAL, "null context");
-    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
+extern "C++" {
+namespace {
+// Shared by the sharded solves: clip every query to this shard (k_shard_local),
+// run the ordinary single-device solve `local` on the shard, turn its local
+// answers into packed keys with global positions (k_shard_keys).
+template <class Local>
+int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset, uint64_t n_total,
+                const brmq_query* Q, uint64_t q, uint64_t* keys, uint32_t flags, Local local) {
     if (n_total > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     if (n_shard == 0 || offset + n_shard > n_total)
         return fail(BRMQ_EINVAL, "shard [%llu, %llu) outside the array of %llu",
@@ -546,8 +549,7 @@ int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint6
     CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
     const unsigned g = unsigned((q + 255) / 256);
     k_shard_local<<<g, 256, 0, s>>>(dQ, q, offset, n_shard, n_total, Ql, empty, err);
-    int rc = brmq_solve_bbst(c, dA, n_shard, reinterpret_cast<const brmq_query*>(Ql), q, k, loc,
-                             BRMQ_PTR_DEVICE);
+    int rc = local(dA, reinterpret_cast<const brmq_query*>(Ql), loc);
     if (rc == BRMQ_OK) {
         k_shard_keys<<<g, 256, 0, s>>>(loc, empty, dA, offset, q, dev ? keys : dkeys);
         uint32_t herr = 0;
@@ -560,6 +562,33 @@ int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint6
     cudaFreeAsync(buf, s);
     CUDA_TRY(cudaStreamSynchronize(s));
     return rc;
+}
+}  // namespace
+}  // extern "C++"
+
+int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset,
+                          uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
+                          uint64_t* keys, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
+    return solve_shard(c, A, n_shard, offset, n_total, Q, q, keys, flags,
+                       [&](const int32_t* dA, const brmq_query* Ql, uint64_t* loc) {
+                           return brmq_solve_bbst(c, dA, n_shard, Ql, q, k, loc, BRMQ_PTR_DEVICE);
+                       });
+}
+
+int brmq_solve_bbst_con_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset,
+                              uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
+                              int sort_kind, uint64_t* keys, uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst_con: block size k must be >= 1");
+    // the clipped queries' endpoints include the shard borders of every query that
+    // crosses one: the shard is contracted with its own endpoints plus those borders
+    return solve_shard(c, A, n_shard, offset, n_total, Q, q, keys, flags,
+                       [&](const int32_t* dA, const brmq_query* Ql, uint64_t* loc) {
+                           return brmq_solve_bbst_con(c, dA, n_shard, Ql, q, k, sort_kind, loc,
+                                                      BRMQ_PTR_DEVICE);
+                       });
 }
 
 // ------------------------------------------------------------------ naive

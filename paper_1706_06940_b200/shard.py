@@ -46,7 +46,14 @@ def allreduce_min_keys(keys: np.ndarray, group=None) -> np.ndarray:
     return from_signed(t.numpy())
 
 
-def solve_sharded(engine, shard, batch, offset: int, n_total: int, k: int = 512, group=None):
-    """This rank's part of a sharded solve plus the combine: answers for all queries."""
-    keys = engine.solve_batch_bbst_shard(shard, batch, offset, n_total, k)
+def solve_sharded(engine, shard, batch, offset: int, n_total: int, k: int = 512, group=None,
+                  contraction: bool = False, sort_kind=None):
+    """This rank's part of a sharded solve plus the combine: answers for all queries.
+    contraction=True solves the shard with BbST_CON (contraction variant)."""
+    if contraction:
+        from .batchrmq import SortKind
+        keys = engine.solve_batch_bbst_con_shard(shard, batch, offset, n_total, k,
+                                                 SortKind.Bitmap if sort_kind is None else sort_kind)
+    else:
+        keys = engine.solve_batch_bbst_shard(shard, batch, offset, n_total, k)
     return keys_to_answers(allreduce_min_keys(np.asarray(keys, np.uint64), group))

@@ -3,8 +3,9 @@
 CPU (gloo, world_size 2): the host side -- shard bounds, key packing, the
 order-preserving signed mapping and the min-allreduce -- with each rank's
 per-shard keys computed by a numpy stand-in of brmq_solve_bbst_shard.
-GPU: the device shard solve itself, three shards on one device combined with a
-plain minimum, bit-exact against the oracle.
+GPU: the device shard solves (BbST, and BbST_CON with either endpoint sort),
+three shards on one device combined with a plain minimum, bit-exact against the
+oracle.
 """
 import os
 import socket
@@ -14,6 +15,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import oracle
+from paper_1706_06940_b200 import SortKind
 from paper_1706_06940_b200 import shard as S
 
 
@@ -89,7 +91,8 @@ def test_shard_bounds_cover():
 
 
 @pytest.mark.gpu
-def test_shard_solve_gpu(engine, orc):
+@pytest.mark.parametrize("variant", ["bbst", "con_bitmap", "con_radix"])
+def test_shard_solve_gpu(engine, orc, variant):
     r = np.random.default_rng(8)
     n = 200_003
     A = r.integers(0, 1000, n).astype(np.int32)
@@ -104,7 +107,11 @@ def test_shard_solve_gpu(engine, orc):
         keys = np.full(Q.shape[0], S.NO_KEY, np.uint64)
         for rank in range(world):
             off, ns = S.shard_bounds(n, world, rank)
-            kr = engine.solve_batch_bbst_shard(A[off:off + ns], Q, off, n, 512)
+            if variant == "bbst":
+                kr = engine.solve_batch_bbst_shard(A[off:off + ns], Q, off, n, 512)
+            else:  # SURVEY 8e contraction variant: shard borders become boundaries
+                sk = SortKind.Bitmap if variant == "con_bitmap" else SortKind.Radix
+                kr = engine.solve_batch_bbst_con_shard(A[off:off + ns], Q, off, n, 512, sk)
             if rank == 1:  # spot-check the per-shard keys against the stand-in
                 assert np.array_equal(kr[:300], shard_keys_reference(A, Q[:300], off, ns))
             keys = np.minimum(keys, kr)
