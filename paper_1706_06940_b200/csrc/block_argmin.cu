@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys_ml(
     uint32_t k, uint64_t* __restrict__ keys, uint64_t* __restrict__ sub,
     uint64_t* __restrict__ b_dev) {
     const uint64_t len = len_dev ? *len_dev : len_max;
-    const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const uint64_t blk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
     const uint64_t lo = blk * k;
     if (lo >= len) return;
@@ -293,8 +293,10 @@ int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint6
                                 cudaStream_t stream) {
     uint64_t nblk = (len_max + k - 1) / k;
     if (nblk == 0) nblk = 1;  // still publish *b_dev
-    k_block_argmin_keys_ml<<<grid_for_warps(nblk), kThreads, 0, stream>>>(K, len_dev, len_max, k,
-                                                                          keys, sub, b_dev);
+    // few blocks (A_Q of a small batch): one warp per CTA spreads them over all SMs
+    const unsigned nt = nblk <= uint64_t(148) * 32 ? 32u : unsigned(kThreads);
+    k_block_argmin_keys_ml<<<unsigned((nblk * 32 + nt - 1) / nt), nt, 0, stream>>>(K, len_dev, len_max,
+                                                                                 k, keys, sub, b_dev);
     return 1;
 }
 
