@@ -54,6 +54,10 @@ struct Endpoint {  // contraction.hpp:12-21
 
 enum class SortKind { Radix, Comparison };  // contraction.hpp:23
 
+struct ContractionStats {  // contraction.hpp:47-49
+    std::uint64_t array_reads{0};
+};
+
 struct ContractedArray {  // contraction.hpp:28-34
     std::vector<Value> aq_values;
     std::vector<Index> aq_origin;
@@ -136,10 +140,12 @@ inline void sort_endpoints(std::vector<Endpoint>& endpoints, SortKind kind = Sor
                                     BRMQ_PTR_HOST));
 }
 
-// contraction.hpp:61-64 (threads / stats accepted for source compatibility)
+// contraction.hpp:61-64.  `threads` has no device meaning; `stats` receives the
+// reads of `values` the device made: every position of [b_0, b_last] once, the
+// count of the reference's serial path (contraction.cpp:85-105, 133-139).
 inline ContractedArray build_contracted(std::span<const Value> values,
                                         const std::vector<Endpoint>& sorted_endpoints,
-                                        unsigned /*threads*/ = 1, void* /*stats*/ = nullptr) {
+                                        unsigned /*threads*/ = 1, ContractionStats* stats = nullptr) {
     const std::size_t m = sorted_endpoints.size();
     ContractedArray out;
     out.aq_values.resize(m);
@@ -154,6 +160,20 @@ inline ContractedArray build_contracted(std::span<const Value> values,
     out.aq_values.resize(areas);
     out.aq_origin.resize(areas);
     out.boundary.resize(nb);
+    if (stats && areas > 0) stats->array_reads += out.boundary.back() - out.boundary.front() + 1;
+    return out;
+}
+
+// contraction.hpp:67 (contraction.cpp:152-171): binary search per query end
+inline ContractedQueryBatch remap_queries(const QueryBatch& batch, const ContractedArray& contracted) {
+    const std::size_t q = batch.size();
+    std::vector<std::uint32_t> cl(q), cr(q);
+    std::vector<std::uint8_t> dg(q);
+    b200::check(brmq_remap_queries(b200::context().get(), reinterpret_cast<const brmq_query*>(batch.data()),
+                                   q, contracted.boundary.data(), contracted.boundary.size(), cl.data(),
+                                   cr.data(), dg.data(), BRMQ_PTR_HOST));
+    ContractedQueryBatch out(q);
+    for (std::size_t i = 0; i < q; ++i) out[i] = {cl[i], cr[i], dg[i] != 0};
     return out;
 }
 

@@ -169,6 +169,14 @@ int brmq_remap_from_sorted(brmq_ctx* ctx, const brmq_endpoint* sorted_eps, uint6
                            const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cleft,
                            uint32_t* cright, uint8_t* degenerate, uint32_t flags);
 
+/* contraction.hpp:67 remap_queries (contraction.cpp:152-171): per query, the
+ * boundary index of each end by binary search (cleft = index(left), cright =
+ * index(right) - 1); a degenerate query (left == right) keeps cleft = cright = 0.
+ * An end missing from the boundary list -> BRMQ_ELOGIC. */
+int brmq_remap_queries(brmq_ctx* ctx, const brmq_query* Q, uint64_t q, const uint64_t* boundary,
+                       uint64_t nb, uint32_t* cleft, uint32_t* cright, uint8_t* degenerate,
+                       uint32_t flags);
+
 /* SPEC.md:210-218 build_block_sparse(values, k): table[e*b + j] (b = ceil(m/k),
  * levels = floor_log2(b)+1, table sized levels*b) = position of the leftmost
  * minimum over blocks j .. j+2^e-1; cells whose span does not fit are

@@ -36,6 +36,7 @@ _PORT_SIGS = {
     "orc_sort_endpoints": (C.c_int, [vp, C.c_uint64, C.c_int]),
     "orc_build_contracted": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, C.c_uint, vp, vp, vp, u64p,
                                        u64p]),
+    "orc_remap_queries": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp]),
     "orc_remap_from_sorted": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, vp, vp, vp]),
     "orc_solve_oracle": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, C.c_uint, vp]),
     "orc_build_block_sparse": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp, u64p, u32p]),

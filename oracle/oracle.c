@@ -306,6 +306,35 @@ int orc_remap_from_sorted(const uint32_t* sorted_eps, uint64_t m, const uint64_t
     return OK;
 }
 
+/* contraction.cpp:152-171 remap_queries: lower_bound of each end of every query
+ * in the boundary list (queries normalised left <= right, types.hpp:18-20); a
+ * degenerate query keeps cleft = cright = 0 (:163-166); a missing end is a
+ * logic_error (:157-158). */
+int orc_remap_queries(const uint64_t* Q, uint64_t q, const uint64_t* boundary, uint64_t nb,
+                      uint32_t* cleft, uint32_t* cright, uint8_t* degenerate) {
+    for (uint64_t i = 0; i < q; ++i) {
+        const uint64_t a = Q[2 * i], b = Q[2 * i + 1];
+        const uint64_t l = a < b ? a : b, r = a < b ? b : a;
+        cleft[i] = cright[i] = 0;
+        degenerate[i] = 0;
+        if (l == r) { degenerate[i] = 1; continue; }
+        uint64_t idx[2];
+        for (int e = 0; e < 2; ++e) {
+            const uint64_t p = e ? r : l;
+            uint64_t lo = 0, hi = nb;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if (boundary[mid] < p) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= nb || boundary[lo] != p) return ELOGIC_;
+            idx[e] = lo;
+        }
+        cleft[i] = (uint32_t)idx[0];
+        cright[i] = (uint32_t)(idx[1] - 1);
+    }
+    return OK;
+}
+
 /* SURVEY 8c oracle pipeline, made of the restated reference stages. */
 int orc_solve_oracle(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q,
                      unsigned threads, uint64_t* answers) {

@@ -65,6 +65,8 @@ int orc_build_contracted(const int32_t* A, uint64_t n, const uint32_t* sorted_ep
                          unsigned threads, int32_t* aq_values, uint64_t* aq_origin,
                          uint64_t* boundary, uint64_t* nb, uint64_t* reads);
 /* contraction.cpp:174-199 */
+int orc_remap_queries(const uint64_t* Q, uint64_t q, const uint64_t* boundary, uint64_t nb,
+                      uint32_t* cleft, uint32_t* cright, uint8_t* degenerate);
 int orc_remap_from_sorted(const uint32_t* sorted_eps, uint64_t m, const uint64_t* boundary,
                           uint64_t nb, uint64_t q, uint32_t* cleft, uint32_t* cright,
                           uint8_t* degenerate);

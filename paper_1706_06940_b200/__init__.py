@@ -8,5 +8,6 @@ reference operator API (batchrmq.py).
 from .batchrmq import (  # noqa: F401
     ENDPOINT_DTYPE, QUERY_DTYPE, ContractedArray, ContractedQueryBatch, CudaError, DomainError,
     Engine, InvalidArgument, LogicError, OutOfRange, SortKind, build_block_sparse,
-    build_contracted, collect_endpoints, floor_log2, make_queries, remap_queries_from_sorted,
+    build_contracted, collect_endpoints, floor_log2, make_queries, remap_queries,
+    remap_queries_from_sorted,
     solve_batch_bbst, solve_batch_bbst_con, sort_endpoints)

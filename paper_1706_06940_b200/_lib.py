@@ -58,6 +58,7 @@ SIGNATURES = {
     "brmq_sort_endpoints": (C.c_int, [vp, vp, C.c_uint64, C.c_int, C.c_uint32]),
     "brmq_build_contracted": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, u64p,
                                         C.c_uint32]),
+    "brmq_remap_queries": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, C.c_uint32]),
     "brmq_remap_from_sorted": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, vp, vp,
                                          vp, C.c_uint32]),
     "brmq_build_block_sparse": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32, vp, u64p,

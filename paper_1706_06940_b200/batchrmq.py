@@ -288,6 +288,19 @@ class Engine:
                                               _ptr(dg), 0))
         return ContractedQueryBatch(cl, cr, dg.astype(bool))
 
+    def remap_queries(self, batch, contracted: ContractedArray) -> ContractedQueryBatch:
+        """contraction.hpp:67 (contraction.cpp:152-171): binary search of both ends of
+        every query in the boundary list; degenerate queries keep cleft = cright = 0."""
+        batch = _as_queries(batch)
+        b = np.ascontiguousarray(contracted.boundary, dtype=np.uint64)
+        q = batch.shape[0]
+        cl = np.zeros(q, dtype=np.uint32)
+        cr = np.zeros(q, dtype=np.uint32)
+        dg = np.zeros(q, dtype=np.uint8)
+        _check(self._L.brmq_remap_queries(self._h, _ptr(batch), q, _ptr(b), b.shape[0], _ptr(cl),
+                                          _ptr(cr), _ptr(dg), 0))
+        return ContractedQueryBatch(cl, cr, dg.astype(bool))
+
     def build_block_sparse(self, values, k: int):
         """SPEC.md:210-218; returns (table[levels, b] of positions, b, levels)."""
         values = np.ascontiguousarray(values, dtype=np.int32)
@@ -344,6 +357,10 @@ def build_contracted(values, sorted_eps):
 
 def remap_queries_from_sorted(sorted_eps, contracted, query_count):
     return default_engine().remap_queries_from_sorted(sorted_eps, contracted, query_count)
+
+
+def remap_queries(batch, contracted):
+    return default_engine().remap_queries(batch, contracted)
 
 
 def build_block_sparse(values, k):

@@ -1321,6 +1321,45 @@ int brmq_remap_from_sorted(brmq_ctx* c, const brmq_endpoint* sorted_eps, uint64_
     return map_err(c->ctl_host->err);
 }
 
+int brmq_remap_queries(brmq_ctx* c, const brmq_query* Q, uint64_t q, const uint64_t* boundary,
+                       uint64_t nb, uint32_t* cleft, uint32_t* cright, uint8_t* degenerate,
+                       uint32_t flags) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (q == 0) return BRMQ_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_b = dev ? 0 : cv.add(nb * 8);
+    const size_t i_cl = dev ? 0 : cv.add(q * 4), i_cr = dev ? 0 : cv.add(q * 4);
+    const size_t i_dg = dev ? 0 : cv.add(q);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    cudaStream_t s = c->stream;
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    const uint64_t* dB = dev ? boundary : reinterpret_cast<uint64_t*>(P(i_b));
+    uint32_t* dcl = dev ? cleft : reinterpret_cast<uint32_t*>(P(i_cl));
+    uint32_t* dcr = dev ? cright : reinterpret_cast<uint32_t*>(P(i_cr));
+    uint8_t* ddg = dev ? degenerate : reinterpret_cast<uint8_t*>(P(i_dg));
+    c->ctl_clean = false;  // stage calls leave the header dirty
+    CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
+    if (!dev) {
+        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+        if (nb) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dB), boundary, nb * 8, cudaMemcpyHostToDevice, s));
+    }
+    brmq::launch_remap_queries(dQ, q, dB, nb, dcl, dcr, ddg, &ctl->err, s);
+    if (int rc = check_status(c)) return rc;
+    if (!dev) {
+        CUDA_TRY(cudaMemcpyAsync(cleft, dcl, q * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(cright, dcr, q * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(degenerate, ddg, q, cudaMemcpyDeviceToHost, s));
+    }
+    if (int rc = sync_and_read_control(c, ctl)) return rc;
+    return map_err(c->ctl_host->err);
+}
+
 int brmq_build_block_sparse(brmq_ctx* c, const int32_t* values, uint64_t m, uint32_t k,
                             uint64_t* table, uint64_t* b_out, uint32_t* levels_out, uint32_t flags) {
     if (!c || !b_out || !levels_out) return fail(BRMQ_EINVAL, "null argument");

@@ -274,6 +274,42 @@ __global__ void k_remap_finish(uint64_t q, const uint32_t* __restrict__ cl, uint
     if (cr[i] == cl[i]) dg[i] = 1;  // contraction.cpp:191-197
     else { dg[i] = 0; cr[i] -= 1; }
 }
+// remap_queries (contraction.cpp:152-171): per query, lower_bound of each end in
+// the boundary list; a degenerate query (left == right) keeps cleft = cright = 0;
+// an end missing from the list -> err |= 8 (logic_error).  Queries are
+// normalised left <= right first (the Query constructor, types.hpp:18-20).
+__global__ void k_remap_queries(const ulonglong2* __restrict__ Q, uint64_t q,
+                                const uint64_t* __restrict__ boundary, uint64_t nb,
+                                uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
+                                uint8_t* __restrict__ dg, uint32_t* __restrict__ err) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= q) return;
+    const ulonglong2 x = __ldg(Q + i);
+    const uint64_t l = x.x < x.y ? x.x : x.y, r = x.x < x.y ? x.y : x.x;
+    if (l == r) {
+        cl[i] = cr[i] = 0;
+        dg[i] = 1;
+        return;
+    }
+    uint64_t idx[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const uint64_t p = e ? r : l;
+        uint64_t lo = 0, hi = nb;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (__ldg(boundary + mid) < p) lo = mid + 1; else hi = mid;
+        }
+        if (lo >= nb || __ldg(boundary + lo) != p) {
+            atomicOr(err, 8u);
+            return;
+        }
+        idx[e] = lo;
+    }
+    cl[i] = uint32_t(idx[0]);
+    cr[i] = uint32_t(idx[1] - 1);
+    dg[i] = 0;
+}
 __global__ void k_keys_to_pos(uint64_t* __restrict__ t, uint64_t count) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < count) t[i] = t[i] == kNoKey ? ~0ull : uint64_t(key_pos(t[i]));
@@ -452,6 +488,13 @@ int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
         ++l;
     }
     return l;
+}
+int launch_remap_queries(const uint64_t* Q, uint64_t q, const uint64_t* boundary, uint64_t nb,
+                         uint32_t* cl, uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s) {
+    if (!q) return 0;
+    k_remap_queries<<<g256(q), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, boundary, nb,
+                                             cl, cr, dg, err);
+    return 1;
 }
 int launch_marked_fill(const int32_t* A, const uint32_t* boundary, const uint64_t* m_dev,
                        uint64_t m_max, uint64_t* E, cudaStream_t s) {

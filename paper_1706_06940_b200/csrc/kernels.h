@@ -130,6 +130,9 @@ int launch_split_aq(const uint64_t* aq, const uint64_t* len, uint64_t len_max, i
                     uint64_t* origin, cudaStream_t s);
 int launch_u32_to_u64(const uint32_t* a, const uint64_t* len, uint64_t len_max, uint64_t* out,
                       cudaStream_t s);
+// remap_queries (contraction.cpp:152-171): binary search of both ends per query.
+int launch_remap_queries(const uint64_t* Q, uint64_t q, const uint64_t* boundary, uint64_t nb,
+                         uint32_t* cl, uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s);
 int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
                         const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cl,
                         uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s);

@@ -251,6 +251,12 @@ def test_stage_contract_remap(engine, orc):
         assert np.array_equal(cq.cleft, cl)
         assert np.array_equal(cq.cright, cr)
         assert np.array_equal(cq.degenerate, dg.astype(bool))
+        # remap_queries: binary search per query (contraction.cpp:152-171)
+        bq = engine.remap_queries(Q, con)
+        orc.port().orc_remap_queries(orc._p(Q), q, orc._p(bnd), nbv, orc._p(cl), orc._p(cr),
+                                     orc._p(dg))
+        assert np.array_equal(bq.cleft, cl) and np.array_equal(bq.cright, cr)
+        assert np.array_equal(bq.degenerate, dg.astype(bool))
 
 
 def test_stage_contract_errors(engine):
@@ -268,6 +274,8 @@ def test_stage_contract_errors(engine):
     bad = ContractedArray(np.zeros(0, np.int32), np.zeros(0, np.uint64), np.array([3], np.uint64))
     with pytest.raises(LogicError):
         engine.remap_queries_from_sorted(e, bad, 1)
+    with pytest.raises(LogicError):  # contraction.cpp:157-158
+        engine.remap_queries(make_queries([3], [5]), bad)
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 32, 512])

@@ -246,3 +246,32 @@ def test_error_codes():
     bad_boundary = np.array([3], np.uint64)
     cl, cr, dg = np.empty(1, np.uint32), np.empty(1, np.uint32), np.empty(1, np.uint8)
     assert L.orc_remap_from_sorted(P(sorted_eps), 2, P(bad_boundary), 1, 1, P(cl), P(cr), P(dg)) == 4
+
+
+def test_remap_queries_binary_search():
+    """contraction.cpp:152-171 remap_queries: SPEC worked instance, agreement with the
+    merge walk (remap_queries_from_sorted) on non-degenerate queries of the golden
+    fixtures, a missing end -> logic_error, and the compiled reference when present."""
+    L = port()
+    bnd = np.array([1, 3, 4, 6], np.uint64)  # SPEC.md:170-172
+    Q = _q([[1, 4], [6, 3], [2, 2]])
+    cl, cr, dg = np.empty(3, np.uint32), np.empty(3, np.uint32), np.empty(3, np.uint8)
+    assert L.orc_remap_queries(P(Q), 3, P(bnd), 4, P(cl), P(cr), P(dg)) == 0
+    assert list(cl) == [0, 1, 0] and list(cr) == [1, 2, 0] and list(dg) == [0, 0, 1]
+    assert L.orc_remap_queries(P(_q([[0, 4]])), 1, P(bnd), 4, P(cl), P(cr), P(dg)) == 4
+    cases = np.load(GOLD / "ref_cases.npz")
+    for c in [str(x).split(":")[0] for x in cases["cases"]]:
+        Q, b = cases[f"{c}_Q"], cases[f"{c}_boundary"]
+        q = Q.shape[0]
+        cl, cr, dg = np.empty(q, np.uint32), np.empty(q, np.uint32), np.empty(q, np.uint8)
+        assert L.orc_remap_queries(P(Q), q, P(b), b.shape[0], P(cl), P(cr), P(dg)) == 0
+        keep = cases[f"{c}_degenerate"] == 0
+        assert np.array_equal(dg, cases[f"{c}_degenerate"]), c
+        assert np.array_equal(cl[keep], cases[f"{c}_cleft"][keep]), c
+        assert np.array_equal(cr[keep], cases[f"{c}_cright"][keep]), c
+        assert not cl[~keep].any() and not cr[~keep].any(), c
+        if oracle.ref_available():
+            rl, rr, rd = np.empty(q, np.uint32), np.empty(q, np.uint32), np.empty(q, np.uint8)
+            assert oracle.ref().ref_remap_queries(P(Q), q, P(b), b.shape[0], P(rl), P(rr), P(rd)) == 0
+            assert np.array_equal(rl, cl) and np.array_equal(rr, cr) and np.array_equal(rd, dg), c
+
