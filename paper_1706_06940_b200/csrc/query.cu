@@ -62,6 +62,24 @@ struct ElemI32 {
         if (p + 3 >= lo && p + 3 <= hi) b = kmin(b, pack_key(x.w, uint32_t(p + 3)));
         return b;
     }
+    // Lane accumulator over the lane's vectors in increasing position order: a
+    // value and its position in 32-bit registers (strict '<' keeps the leftmost),
+    // one packed key at the end.  Positions fit 32 bits (n <= 2^32 - 1).
+    struct Acc {
+        int32_t bv = 0x7FFFFFFF;
+        uint32_t bi = 0xFFFFFFFFu;  // none yet
+        __device__ __forceinline__ void add(const vec_t& x, uint32_t v, uint32_t lo, uint32_t span) {
+            const uint32_t p = v * 4;
+            const int32_t e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (p + t - lo <= span && (e[t] < bv || bi == 0xFFFFFFFFu)) {  // p + t in [lo, lo + span]
+                    bv = e[t];
+                    bi = p + t;
+                }
+        }
+        __device__ __forceinline__ uint64_t key() const { return bi == 0xFFFFFFFFu ? kNoKey : pack_key(bv, bi); }
+    };
 };
 
 struct ElemKey {
@@ -80,6 +98,15 @@ struct ElemKey {
         if (p + 1 >= lo && p + 1 <= hi) b = kmin(b, (uint64_t(x.w) << 32) | x.z);
         return b;
     }
+    struct Acc {
+        uint64_t b = kNoKey;
+        __device__ __forceinline__ void add(const vec_t& x, uint32_t v, uint32_t lo, uint32_t span) {
+            const uint32_t p = v * 2;
+            if (p - lo <= span) b = kmin(b, (uint64_t(x.y) << 32) | x.x);
+            if (p + 1 - lo <= span) b = kmin(b, (uint64_t(x.w) << 32) | x.z);
+        }
+        __device__ __forceinline__ uint64_t key() const { return b; }
+    };
 };
 
 // A query resolved to index coordinates [il, ir] of the scanned array and
@@ -156,15 +183,18 @@ __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64
 // VPL vectors per lane cover one block (k = 32 * EPV * VPL); TPR ranges per round.
 // WPQ: one warp per query (small batches: the per-warp rounds of partial scans
 // are the latency chain, so spread the queries over 32x more warps).
-template <class E, class QP, int VPL, int TPR, bool WPQ = false>
-__global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
-                                                    const uint64_t* __restrict__ ST,
-                                                    uint64_t stride, uint64_t q,
-                                                    uint64_t* __restrict__ answers,
-                                                    const CtlPublish pub) {
+template <class E, class QP, int VPL, int TPR, bool WPQ = false, int NT = kThreads>
+__global__ void __launch_bounds__(NT) k_query(E elem, QP qp, uint32_t k_rt,
+                                              const uint64_t* __restrict__ ST,
+                                              uint64_t stride, uint64_t q,
+                                              uint64_t* __restrict__ answers,
+                                              const CtlPublish pub) {
+    // the vectorised instances know k at compile time (k = 32 * EPV * VPL): block
+    // indices by shifts, not 64-bit divisions
+    const uint32_t k = VPL > 0 ? uint32_t(32 * E::EPV * (VPL > 0 ? VPL : 1)) : k_rt;
     const unsigned lane = lane_id();
-    const uint64_t i = WPQ ? (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5
-                           : (uint64_t(blockIdx.x) * kThreads + threadIdx.x);
+    const uint64_t i = WPQ ? (uint64_t(blockIdx.x) * NT + threadIdx.x) >> 5
+                           : (uint64_t(blockIdx.x) * NT + threadIdx.x);
     const bool active = i < q && (!WPQ || lane == 0);
 
     uint64_t best = kNoKey, direct = 0;
@@ -242,15 +272,17 @@ __global__ void __launch_bounds__(kThreads) k_query(E elem, QP qp, uint32_t k,
 #pragma unroll
             for (int u = 0; u < TPR; ++u) {
                 if (src[u] < 0) break;  // warp-uniform
-                const uint64_t vb = (tlo[u] / k) * (k / EPV);
-                uint64_t kb = kNoKey;
+                const uint32_t vb = uint32_t((tlo[u] / k) * (k / EPV));
+                const uint32_t lo32 = uint32_t(tlo[u]), span = uint32_t(thi[u] - tlo[u]);
+                typename E::Acc acc;
 #pragma unroll
                 for (int j = 0; j < VPL; ++j) {
-                    const uint64_t v = vb + lane + 32 * j;
-                    if (v * EPV + (EPV - 1) >= tlo[u] && v * EPV <= thi[u])
-                        kb = kmin(kb, elem.vec_min(x[u][j], v, tlo[u], thi[u]));
+                    const uint32_t v = vb + lane + 32 * j;
+                    // 32-bit: the dispatch keeps arrays within 2^32 - 4096 positions
+                    // on this path, so no vector of a block wraps
+                    if (v * EPV + (EPV - 1) >= lo32 && v * EPV <= lo32 + span) acc.add(x[u][j], v, lo32, span);
                 }
-                kb = warp_min_key(kb);
+                const uint64_t kb = warp_min_key(acc.key());
                 if (int(lane) == src[u]) best = kmin(best, kb);
             }
         }
@@ -269,14 +301,17 @@ void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint6
         k_query<E, QP, VPL, TPR, true><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans, pub);
         return;
     }
-    const unsigned grid = unsigned((q + kThreads - 1) / kThreads);
-    k_query<E, QP, VPL, TPR><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans, pub);
+    // 128-thread CTAs: a CTA holds its SM slot until its slowest warp is done
+    // (c3 h = 1: 256 -> 128 threads 1.15 -> 1.04 ms; 64 is slower on c5)
+    k_query<E, QP, VPL, TPR, false, 128><<<unsigned((q + 127) / 128), 128, 0, s>>>(e, qp, k, ST, stride,
+                                                                                  q, ans, pub);
 }
 
 template <class QP>
 void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
                   uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
-    const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0;
+    // (the vectorised instances do 32-bit position arithmetic inside a block)
+    const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0 && e.len <= 0xFFFFFFFFull - 4096;
     // one pending range per round: fewer registers -> more resident warps, which
     // beats batching ranges per round on this latency-bound kernel (measured)
     if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
@@ -290,6 +325,8 @@ void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t str
 template <class QP>
 void dispatch_key(ElemKey e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint64_t q,
                   uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
+    // |A_Q| < 2q: the vectorised instances' 32-bit index arithmetic needs 2q + k < 2^32
+    if (2 * q + 4096 > 0xFFFFFFFFull) return launch_q<ElemKey, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s, pub);
     if (k == 512) return launch_q<ElemKey, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (k == 256) return launch_q<ElemKey, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (k == 1024) return launch_q<ElemKey, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s, pub);
