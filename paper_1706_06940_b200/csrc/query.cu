@@ -1,4 +1,3 @@
-#include <cstdlib>
 // query.cu -- speculative query answering over the block Sparse Table (K3).
 //
 // SPEC.md:219-236 (inner_span_min + answer_one), PAPER.md:242-255 (BbST_CON
@@ -11,14 +10,17 @@
 //   single block: stored min if it lies in [l, r], else scan [l, r]
 // All candidates are packed keys, so combining them is an unsigned min.
 //
-// B200 design: one lane per query does the O(1) part (4 random 8-byte ST reads,
-// L2-resident for n = 1e8).  Lanes that need a partial-block scan publish it
-// with __ballot_sync and the whole warp scans TPR pending ranges per round:
-// each lane issues VPL predicated 128-bit loads per range (TPR*VPL = 16
-// vectors in flight per lane), only for vectors that overlap the range, and a
-// redux.sync pair reduces each range to its leftmost-min key, which goes back
-// to the owning lane.  No lane idles on the ~70% of queries that need no
-// scan, and partial ranges cost one coalesced round trip per 4 ranges.
+// B200 design (k_query): one lane per query does the O(1) part (4 random 8-byte
+// ST reads, L2-resident for n = 1e8).  Lanes that need a partial-block scan
+// publish it with __ballot_sync and the whole warp scans the pending ranges, TPR
+// per round: each lane issues VPL predicated 128-bit loads per range (only for
+// vectors that overlap it), folds them into a 32-bit (value, position)
+// accumulator, and a redux.sync pair reduces the range to its leftmost-min key,
+// which goes back to the owning lane.  No lane idles on the queries that need
+// no scan.  With a 32-element sub-block level (multi-level BbST [32, k], and
+// BbST_CON over A_Q for power-of-two k in [64, 512]) k_query_flat answers
+// instead: fixed-shape lane-private descents through the sub-block keys and
+// pooled half-warp row scans (see the comment above ml_flat_group).
 //
 // Two element policies share the kernel: int32 A (key = pack(A[i], i)) for
 // BbST, and packed keys A_Q (key carries the original position, "aq_origin")
