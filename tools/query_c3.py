@@ -8,7 +8,7 @@ for cfg in ('c3', 'c4', 'c5'):
     eng = Engine(0)
     s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
     dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+    from bench import L2Flush; flush = L2Flush(torch, 'cuda')
     for name, f in (('h1', lambda: eng.solve_batch_bbst(dA, dQ, 512)), ('ml', lambda: eng.solve_batch_bbst_ml(dA, dQ, (32, 512)))):
         ms, _, _ = time_solves(eng, torch, s, f, 5, 2, flush, timing=0)
         _, st, _ = time_solves(eng, torch, s, f, 3, 1, flush, timing=1)

@@ -7,7 +7,7 @@ from bench import gen_workload, time_solves, SEED0
 from paper_1706_06940_b200 import Engine, _lib
 eng = Engine(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+from bench import L2Flush; flush = L2Flush(torch, 'cuda')
 res = {}
 A, Q = gen_workload('c1')
 dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()

@@ -7,7 +7,7 @@ from paper_1706_06940_b200 import Engine
 from bench import time_solves
 eng = Engine(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
-flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+from bench import L2Flush; flush = L2Flush(torch, 'cuda')
 res = {}
 for n in (100_000_000, 1_000_000_000, 1 << 30):
     A = torch.randint(0, 2**31 - 1, (n,), dtype=torch.int32, device='cuda')

@@ -11,7 +11,7 @@ L = _lib.lib()
 eng = Engine(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream); eng.set_timing(True)
 dA = torch.from_numpy(A).cuda()
-flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+from bench import L2Flush; flush = L2Flush(torch, 'cuda')
 res = {}
 for q in (1000, 100000, 1000000, 10000000):
     Q = np.empty((q, 2), np.uint64); L.brmq_workload_queries(0, A.shape[0], q, 1706069402, Q.ctypes.data, 0)

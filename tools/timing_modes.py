@@ -11,7 +11,7 @@ eng = Engine(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); eng.set_stream(s.cuda_stream)
 dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()
 dO = torch.empty(Q.shape[0], dtype=torch.int64, device='cuda')
-flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
+from bench import L2Flush; flush = L2Flush(torch, 'cuda')
 res = {}
 for sk in (2, 0):
     for t in (0, 2, 1):
