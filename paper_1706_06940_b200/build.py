@@ -28,6 +28,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                   "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
+# A/B tooling only (tools/ab_variants.sh): extra nvcc flags such as -DBRMQ_KDENSE=2
+NVFLAGS += os.environ.get("BRMQ_NVCC_EXTRA", "").split()
 CXXFLAGS = ["-O3", "-fPIC", "-std=c++17", "-march=x86-64-v2", "-I", str(ROOT / "include")]
 
 

@@ -936,7 +936,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, !use_bitmap, AQ,
                                   &ctl->nb, &ctl->aq_len,
                                   use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
-                                  c->epoch_dev, 0, s, false, use_bitmap ? pcnt : nullptr);
+                                  c->epoch_dev, 0, s, false, use_bitmap ? pcnt : nullptr, 2 * q);
         launches += l;
         tm.end(l);
         // (bitmap pipeline: the query remap is folded into the query kernel)
@@ -1085,7 +1085,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         tm.stage("contract", launches);
         l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, true, ST, &ctl->nb,
                                   &ctl->aq_len, nullptr, S(i_cst), c->epoch_dev, 0, s,
-                                  /*marked=*/true);
+                                  /*marked=*/true, nullptr, 2 * q);
         l += brmq::launch_marked_fill(dA, bd, &ctl->nb, m, ST, s);
         l += brmq::launch_marked_edges(dA, n, ctl->span, &ctl->nb, ST, s);
         launches += l;

@@ -57,7 +57,14 @@ constexpr int kRow = 32;            // positions per lane = one 128-byte row
 constexpr int kWTile = 32 * kRow;   // 1024 positions = 4 KB per warp tile
 constexpr int kTile = 4 * kWTile;   // 4096: the partition unit
 static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
-constexpr int kDense = 4;           // flagged rows per warp tile above which rows close per lane
+#ifndef BRMQ_KDENSE
+#define BRMQ_KDENSE 4
+#endif
+#ifndef BRMQ_CONTRACT_MINB
+#define BRMQ_CONTRACT_MINB 2  // 2 CTAs per SM: <= 128 registers (129 would halve the residency)
+#endif
+constexpr int kDense = BRMQ_KDENSE;  // flagged rows per warp tile above which rows close per lane
+constexpr int kDenseEndpoints = 8;  // endpoints per warp tile from which only dense rows are compiled in
 
 // Rows of the current warp tile in the warp's swizzled shared rows (16-byte
 // chunk c of row r at byte r*128 + ((c ^ (r & 7)) << 4)), read with explicit
@@ -291,8 +298,11 @@ struct ContractArgs {
 
 // MARKED: ST-RMQ_CON's marked contraction -- marked positions read as +inf
 // inside the areas (they get their own entries) and areas go to aq_slot.
-template <bool VEC, bool MARKED>
-__global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ ContractArgs c) {
+// SPARSE = false: every warp tile holding a boundary takes the dense one-pass
+// rows (the instance for high boundary densities: without the sparse path
+// compiled in, c5-con's contraction runs 5% faster).
+template <bool VEC, bool MARKED, bool SPARSE = true>
+__global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
     __shared__ __align__(128) int4 s_rows[NW][kWTile / 4];  // per warp: 32 rows x 128 B, swizzled
     __shared__ uint32_t s_cnt[NW];
     __shared__ uint64_t s_tail[NW];
@@ -330,6 +340,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             const int4* A4 = reinterpret_cast<const int4*>(c.A + tile_lo);
 #pragma unroll
             for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(A4 + u * 32 + lane);
+
         } else {  // array tail / unaligned A: scalar loads, positions >= n read as 0 (masked later)
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(NT) k_contract(const __grid_constant__ Contrac
             carry.k = kmin(carry.k, key);
             return;
         }
-        const bool dense = __popc(fm) > kDense;
+        const bool dense = !SPARSE || __popc(fm) > kDense;
 
         // pass 1: open-segment key at the right end of the lane's row; a dense
         // tile's flagged rows are handled in one pass below instead
@@ -689,7 +700,8 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out,
                     uint64_t* aq_len,
                     uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
-                    uint32_t epoch_off, cudaStream_t s, bool marked, const uint32_t* pcnt) {
+                    uint32_t epoch_off, cudaStream_t s, bool marked, const uint32_t* pcnt,
+                    uint64_t endpoints) {
     if (n == 0) return 0;
     uint32_t G = 0, R = 0;
     contract_partition(n, &G, &R);
@@ -698,8 +710,13 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                       epoch_off};
     void* params[] = {&args};
     const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
-    const void* fn = vec ? (marked ? reinterpret_cast<const void*>(k_contract<true, true>)
-                                   : reinterpret_cast<const void*>(k_contract<true, false>))
+    // >= 8 endpoints per 1024 positions on average: nearly every flagged warp tile
+    // has more than kDense flagged rows, so the dense-only instance runs
+    const bool dense = endpoints >= uint64_t(kDenseEndpoints) * (n / kWTile + 1);
+    const void* fn = vec ? (marked ? (dense ? reinterpret_cast<const void*>(k_contract<true, true, false>)
+                                            : reinterpret_cast<const void*>(k_contract<true, true>))
+                                   : (dense ? reinterpret_cast<const void*>(k_contract<true, false, false>)
+                                            : reinterpret_cast<const void*>(k_contract<true, false>)))
                          : (marked ? reinterpret_cast<const void*>(k_contract<false, true>)
                                    : reinterpret_cast<const void*>(k_contract<false, false>));
     cudaLaunchCooperativeKernel(fn,

@@ -119,7 +119,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
                     cudaStream_t s, bool marked = false,
-                    const uint32_t* pcnt = nullptr);
+                    const uint32_t* pcnt = nullptr, uint64_t endpoints = 0);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)
