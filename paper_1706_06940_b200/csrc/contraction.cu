@@ -467,21 +467,15 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
         uint64_t run = kNoKey;
         if (any && fl == 0 && (GEN || !dense))  // (dense interior tiles: row_pass_all below)
             run = !GEN ? row_min<true>(rs, lane, 0, kRow - 1) : row_min<false>(rs, lane, jlo, jhi);
-        uint64_t hd = kNoKey;  // single-boundary row: min over [jlo, boundary], carry excluded
         if (!dense) {  // sparse flagged rows: one element per lane
             for (unsigned m = fm; m; m &= m - 1) {
                 const int s = __ffs(m) - 1;
                 const uint32_t ft = __shfl_sync(kFull, fl, s);
-                const int jl = __shfl_sync(kFull, jlo, s);
                 const int jh = __shfl_sync(kFull, jhi, s);
                 const int lo = 31 - __clz(ft);
                 const int32_t v = rs.elem(uint32_t(s), int(lane));
                 const uint64_t key = pack_key(v, uint32_t(rs.pos(uint32_t(s), int(lane))));
                 const uint64_t mk = warp_min_key(int(lane) >= lo && int(lane) <= jh ? key : kNoKey);
-                if ((ft & (ft - 1)) == 0) {  // one boundary: its head part now, no scan later
-                    const uint64_t mh = warp_min_key(int(lane) >= jl && int(lane) <= lo ? key : kNoKey);
-                    if (lane == uint32_t(s)) hd = mh;
-                }
                 if (lane == uint32_t(s)) run = mk;
             }
         }
@@ -533,21 +527,33 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
         } else {
             const int L = 31 - __clz(fm);
             wt = SegMin{warp_min_key(int(lane) >= L ? run : kNoKey), 1};
-            wc = __reduce_add_sync(kFull, cntb);
+            // rows holding one boundary each (the common sparse case): ranks are
+            // popcounts of the flagged rows before, no reductions
+            const bool multi = __any_sync(kFull, (fl & (fl - 1)) != 0);
+            wc = multi ? __reduce_add_sync(kFull, cntb) : uint32_t(__popc(fm));
             for (unsigned m = fm; m; m &= m - 1) {
                 const int s = __ffs(m) - 1;
                 const uint32_t ft = __shfl_sync(kFull, fl, s);
+                const int jl = __shfl_sync(kFull, jlo, s);
                 // open segment entering row s: rows after the previous flagged row
                 const unsigned below = fm & ((1u << s) - 1u);
                 const int pf = below ? 31 - __clz(below) : -1;
-                const uint64_t seg = warp_min_key((int(lane) >= (pf < 0 ? 0 : pf) && int(lane) < s) ? run : kNoKey);
-                const SegMin in = pf >= 0 ? SegMin{seg, 1} : seg_combine(carry, SegMin{seg, 0});
-                const uint64_t rank = rank_run + __reduce_add_sync(kFull, int(lane) < s ? cntb : 0u);
+                const int sl = pf < 0 ? 0 : pf;
+                const uint64_t rank =
+                    rank_run + (multi ? __reduce_add_sync(kFull, int(lane) < s ? cntb : 0u) : uint32_t(__popc(below)));
                 if (lane == uint32_t(s)) my_rank = rank;
-                if ((ft & (ft - 1)) == 0) {  // one boundary: area = open segment + head part
+                if ((ft & (ft - 1)) == 0) {
+                    // one boundary at column lo: its area = the open segment entering
+                    // row s + the row's head part [jl, lo], in one reduction
+                    const int lo = 31 - __clz(ft);
+                    uint64_t x = int(lane) >= sl && int(lane) < s ? run : kNoKey;
+                    if (int(lane) >= jl && int(lane) <= lo)
+                        x = kmin(x, pack_key(rs.elem(uint32_t(s), int(lane)),
+                                             uint32_t(rs.pos(uint32_t(s), int(lane)))));
+                    uint64_t val = warp_min_key(x);
+                    if (pf < 0) val = kmin(val, carry.k);
                     if (lane == uint32_t(s)) {
-                        const uint64_t val = kmin(in.k, hd);
-                        if (!in.f) {
+                        if (pf < 0 && !carry.f) {
                             head = val;
                             head_set = true;
                         } else {
@@ -556,7 +562,8 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
                     }
                     continue;
                 }
-                const int jl = __shfl_sync(kFull, jlo, s);
+                const uint64_t seg = warp_min_key(int(lane) >= sl && int(lane) < s ? run : kNoKey);
+                const SegMin in = pf >= 0 ? SegMin{seg, 1} : seg_combine(carry, SegMin{seg, 0});
                 const int jh = __shfl_sync(kFull, jhi, s);
                 const int32_t v = rs.elem(uint32_t(s), int(lane));
                 const bool inr = int(lane) >= jl && int(lane) <= jh;

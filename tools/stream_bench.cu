@@ -177,6 +177,34 @@ __global__ void k_ldg_sts(const int4* __restrict__ a, uint64_t nvec, unsigned* o
     if (lane == 0 && m == 0x12345678) atomicAdd(out, 1u);
 }
 
+// non-persistent, one warp per 4 KB warp tile (8 x 16 B per lane in flight), the
+// contraction's shared-memory transpose, lane r reads row r; residency set by
+// the dynamic shared memory the launch asks for
+__global__ void k_ldg8_sts(const int4* __restrict__ a, uint64_t nvec, unsigned* out) {
+    __shared__ __align__(128) int4 sx[8][256];
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (w * 256 >= nvec) return;
+    int4 y[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(a + w * 256 + u * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t row = 4u * u + (lane >> 3), ch = lane & 7u;
+        sx[warp][row * 8u + (ch ^ (row & 7u))] = y[u];
+    }
+    __syncwarp();
+    int m = 0x7FFFFFFF;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int4 v = sx[warp][lane * 8u + (c ^ (lane & 7u))];
+        m = __vimin3_s32(m, v.x, v.y);
+        m = __vimin3_s32(m, v.z, v.w);
+    }
+    m = __reduce_min_sync(0xffffffffu, m);
+    if (lane == 0 && m == 0x12345678) atomicAdd(out, 1u);
+}
+
 // persistent: CTA c streams contiguous range of tiles; S stages of T bytes.
 template <bool TMA2D>
 __global__ void k_ring(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ a,
@@ -280,6 +308,14 @@ int main(int argc, char** argv) {
         timeit((std::string("ldg+sts warps/sm=") + std::to_string(per * 8)).c_str(), [&] {
             k_ldg_sts<<<sms * per, 256>>>(reinterpret_cast<int4*>(a), nvec, out);
         });
+    for (int per : {2, 3, 4, 8}) {
+        const int smem = (200 * 1024) / per - 32 * 1024 - 1024;  // static 32 KB + dynamic
+        cudaFuncSetAttribute(k_ldg8_sts, cudaFuncAttributeMaxDynamicSharedMemorySize, smem > 0 ? smem : 0);
+        timeit((std::string("ldg8+sts np cta/sm=") + std::to_string(per)).c_str(), [&] {
+            k_ldg8_sts<<<unsigned((nvec / 256 * 32 + 255) / 256), 256, smem > 0 ? smem : 0>>>(
+                reinterpret_cast<int4*>(a), nvec, out);
+        });
+    }
     auto cpa = [&](auto kern, int S, int cpsm) {
         const size_t smem = size_t(8) * S * 2048;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
