@@ -234,7 +234,7 @@ inline Answers solve_batch_naive(std::span<const Value> array, const QueryBatch&
     return out;
 }
 
-// SPEC.md:266-310 with a LevelConfig chain (h = 1, or h = 2 with k_1 = 32)
+// SPEC.md:266-310 with a LevelConfig chain (any dividing chain k_1 < ... < k_h, h <= 8)
 struct LevelConfig {
     std::vector<std::uint32_t> block_sizes{512};
 };

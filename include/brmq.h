@@ -95,11 +95,13 @@ int brmq_solve_bbst(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_quer
                     uint64_t q, uint32_t k, uint64_t* answers, uint32_t flags);
 
 /* SPEC.md:266-310 solve_batch_bbst(array, batch, LevelConfig{k_1 < ... < k_h})
- * -- multi-level BbST.  Supported chains: h = 1 ({k}, same as
- * brmq_solve_bbst) and h = 2 with k_1 = 32 and k_2 a multiple of 32: one pass
- * over A stores the 32-element sub-block minima next to the k_2-block minima,
- * and endpoint blocks are resolved through them (raw A is read only inside one
- * partial sub-block per edge).  Other chains -> BRMQ_EINVAL. */
+ * -- multi-level BbST.  Any dividing chain, 1 <= h <= 8:
+ * h = 1 is brmq_solve_bbst; [32, k] (32 | k) has the specialised path (one pass
+ * over A stores the 32-element sub-block minima next to the k-block minima); any
+ * other chain builds the k_i-block minima level by level from the one below and
+ * answers with one warp per query descending the levels (query_chain.cu).  A
+ * chain that is not strictly ascending with k_i | k_{i+1}, or has h = 0 or h > 8
+ * -> BRMQ_EINVAL ("non-dividing chain -> configuration error"). */
 int brmq_solve_bbst_ml(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_query* Q,
                        uint64_t q, const uint32_t* ks, uint32_t h, uint64_t* answers,
                        uint32_t flags);

@@ -171,7 +171,7 @@ class Engine:
         return self._solve(False, array, batch, k, 0, out)
 
     def solve_batch_bbst_ml(self, array, batch, ks=(32, 512), out=None):
-        """SPEC.md:266-310 with LevelConfig ks (h = 1, or h = 2 with k_1 = 32)."""
+        """SPEC.md:266-310 with LevelConfig ks: any dividing chain k_1 < ... < k_h, h <= 8."""
         return self._solve("ml", array, batch, tuple(int(x) for x in ks), 0, out)
 
     def solve_batch_bbst_con(self, array, batch, k: int = 512,

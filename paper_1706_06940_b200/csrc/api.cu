@@ -731,13 +731,106 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
 }
 
 // ------------------------------------------------------------ multi-level BbST
+// Any other dividing chain (query_chain.cu): M_0 = k_1-block minima of A, M_j from
+// M_{j-1} (k_{j+1}/k_j children each), the k_h-block minima from M_{h-2}, the
+// block Sparse Table over them, one warp per query descending the levels.
+static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
+                const uint32_t* ks, uint32_t h, uint64_t* answers, uint32_t flags) {
+    if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
+    const uint32_t k = ks[h - 1];
+    c->info = brmq_solve_info{};
+    c->info.n = n;
+    c->info.q = q;
+    c->info.k = k;
+    Timer tm(c);
+    if (q == 0) {
+        tm.finish();
+        return BRMQ_OK;
+    }
+    if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const bool dev = is_device(flags);
+    const uint64_t b = (n + k - 1) / k;
+    const uint32_t L = brmq::floor_log2_u64(b) + 1;
+    Carve cv;
+    const size_t i_ctl = cv.add(sizeof(Control));
+    const size_t i_st = cv.add(size_t(L) * b * 8);
+    size_t i_m[brmq::kMaxChain] = {};
+    uint64_t mlen[brmq::kMaxChain] = {};
+    for (uint32_t j = 0; j + 1 < h; ++j) {
+        mlen[j] = (n + ks[j] - 1) / ks[j];
+        i_m[j] = cv.add(mlen[j] * 8);
+    }
+    const size_t i_a = dev ? 0 : cv.add(n * 4);
+    const size_t i_q = dev ? 0 : cv.add(q * 16);
+    const size_t i_ans = dev ? 0 : cv.add(q * 8);
+    if (int rc = ensure_ws(c, cv.total)) return rc;
+    auto P = [&](size_t i) { return c->ws + cv.off[i]; };
+    auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
+    auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
+    uint64_t* M[brmq::kMaxChain] = {};
+    for (uint32_t j = 0; j + 1 < h; ++j) M[j] = reinterpret_cast<uint64_t*>(P(i_m[j]));
+    const int32_t* dA = dev ? A : reinterpret_cast<int32_t*>(P(i_a));
+    const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
+    uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
+    cudaStream_t s = c->stream;
+    int launches = 0;
+    auto enqueue = [&]() -> int {
+        int l = 0;
+        if (!dev) {
+            tm.stage("h2d", launches);
+            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            tm.end(0);
+        }
+        tm.stage("block_argmin", launches);
+        l = brmq::launch_block_argmin_i32(dA, n, ks[0], M[0], s);  // level k_1 from A
+        for (uint32_t j = 1; j + 1 < h; ++j)                       // level k_{j+1} from level k_j
+            l += brmq::launch_block_argmin_keys(M[j - 1], mlen[j - 1], nullptr, ks[j] / ks[j - 1], M[j],
+                                                nullptr, s);
+        l += brmq::launch_block_argmin_keys(M[h - 2], mlen[h - 2], nullptr, k / ks[h - 2], ST, nullptr, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("sparse_table", launches);
+        l = brmq::launch_sparse_table(ST, b, nullptr, s);
+        launches += l;
+        tm.end(l);
+        tm.stage("query", launches);
+        l = brmq::launch_query_chain(dA, n, ks, h, M, ST, b, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
+        launches += l;
+        tm.end(l);
+        if (int rc = check_status(c)) return rc;
+        if (!dev) {
+            tm.stage("d2h", launches);
+            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            tm.end(0);
+        }
+        return BRMQ_OK;
+    };
+    // no graph cache: the key has no room for the chain; a direct enqueue is 4 + h launches
+    const GraphKey key{5, A, n, Q, q, k, int(h), answers, s};
+    if (int rc = prepare_ctl(c, ctl)) return rc;
+    if (int rc = run_solve(c, key, false, tm, launches, enqueue)) return rc;
+    c->ctl_clean = true;  // the final kernel published and re-zeroed the header
+    CUDA_TRY(cudaStreamSynchronize(s));
+    tm.finish();
+    c->info.blocks = b;
+    c->info.levels = L;
+    c->info.kernel_launches = uint32_t(launches);
+    return map_err(c->ctl_host->err);
+}
+
 int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
                        const uint32_t* ks, uint32_t h, uint64_t* answers, uint32_t flags) {
     if (!c || !ks) return fail(BRMQ_EINVAL, "null argument");
+    if (h == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: empty level config");
     if (h == 1) return brmq_solve_bbst(c, A, n, Q, q, ks[0], answers, flags);
-    if (h != 2 || ks[0] != 32 || ks[1] <= 32 || ks[1] % 32 != 0)
-        return fail(BRMQ_EINVAL,
-                    "solve_batch_bbst: supported level configs are [k] and [32, k] with 32 | k");
+    if (h > brmq::kMaxChain) return fail(BRMQ_EINVAL, "solve_batch_bbst: at most 8 levels");
+    for (uint32_t j = 0; j < h; ++j) {  // k_1 < ... < k_h, k_i | k_{i+1}
+        if (ks[j] == 0 || (j > 0 && (ks[j] <= ks[j - 1] || ks[j] % ks[j - 1] != 0)))
+            return fail(BRMQ_EINVAL, "solve_batch_bbst: the level config is not a dividing chain");
+    }
+    if (h != 2 || ks[0] != 32) return solve_chain(c, A, n, Q, q, ks, h, answers, flags);
     const uint32_t k = ks[1];
     if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     c->info = brmq_solve_info{};

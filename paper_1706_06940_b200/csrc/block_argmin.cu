@@ -116,6 +116,75 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys(const uint64_t* 
     if (lane == 0) keys[blk] = best;
 }
 
+// Small blocks (k < 32, the lower levels of a multi-level chain): one thread per
+// block, its k cells read in order (a warp covers 32k contiguous cells, so every
+// sector is fetched once through L1); ascending positions + strict '<' = leftmost.
+__global__ void __launch_bounds__(kThreads) k_block_argmin_i32_small(const int32_t* __restrict__ A,
+                                                                     uint64_t n, uint32_t k,
+                                                                     uint64_t nblk,
+                                                                     uint64_t* __restrict__ keys) {
+    const uint64_t blk = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (blk >= nblk) return;
+    const uint64_t lo = blk * k, hi = lo + k < n ? lo + k : n;
+    int32_t bv = __ldg(A + lo);
+    uint64_t bp = lo;
+    for (uint64_t i = lo + 1; i < hi; ++i) {
+        const int32_t v = __ldg(A + i);
+        if (v < bv) { bv = v; bp = i; }
+    }
+    keys[blk] = pack_key(bv, uint32_t(bp));
+}
+
+__global__ void __launch_bounds__(kThreads) k_block_argmin_keys_small(const uint64_t* __restrict__ K,
+                                                                      uint64_t len, uint32_t k,
+                                                                      uint64_t nblk,
+                                                                      uint64_t* __restrict__ keys) {
+    const uint64_t blk = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
+    if (blk >= nblk) return;
+    const uint64_t lo = blk * k, hi = lo + k < len ? lo + k : len;
+    uint64_t best = kNoKey;
+    for (uint64_t i = lo; i < hi; ++i) best = kmin(best, __ldg(K + i));
+    keys[blk] = best;
+}
+
+// k = 4V, V in {1, 2, 4, 8, 16, 32} (k = 4 .. 128), A 16-byte aligned: one
+// 128-bit vector per lane, V lanes per block, 4 rounds of 32 vectors per warp in
+// flight; the lane-local leftmost minimum of its 4 cells is combined over the
+// V-lane group with shuffles (lower lanes hold lower positions: kmin is leftmost).
+template <int V>
+__global__ void __launch_bounds__(kThreads) k_block_argmin_i32_grp(const int32_t* __restrict__ A,
+                                                                   uint64_t nfull,
+                                                                   uint64_t* __restrict__ keys) {
+    constexpr int kR = 4;
+    const uint64_t warp = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const unsigned lane = lane_id();
+    const int4* A4 = reinterpret_cast<const int4*>(A);
+    const uint64_t nvec = nfull * V;
+    int4 x[kR];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+        const uint64_t v = (warp * kR + u) * 32 + lane;
+        if (v < nvec) x[u] = ld_stream_v4(A4 + v);
+    }
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+        const uint64_t v = (warp * kR + u) * 32 + lane;
+        if ((warp * kR + u) * 32 >= nvec) break;  // warp-uniform
+        uint64_t key = kNoKey;
+        if (v < nvec) {
+            const uint32_t p = uint32_t(v * 4);
+            int32_t bv = x[u].x;
+            uint32_t bp = p;
+            if (x[u].y < bv) { bv = x[u].y; bp = p + 1; }
+            if (x[u].z < bv) { bv = x[u].z; bp = p + 2; }
+            if (x[u].w < bv) { bv = x[u].w; bp = p + 3; }
+            key = pack_key(bv, bp);
+        }
+        key = group_min_key<V>(key);
+        if (v < nvec && lane % V == 0) keys[v / V] = key;
+    }
+}
+
 inline unsigned grid_for_warps(uint64_t warps) {
     return unsigned((warps + kWarps - 1) / kWarps);
 }
@@ -136,7 +205,26 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
         k_pack_keys<<<unsigned((n + 255) / 256), 256, 0, stream>>>(A, n, keys);
         return 1;
     }
-    if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
+    const bool al = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
+    if (al && k <= 128 && (k & (k - 1)) == 0 && k >= 4 && n / k > 0) {
+        const uint64_t nfull = n / k;
+        const unsigned grid = unsigned((nfull * (k / 4) + 32 * 4 * kWarps - 1) / (32 * 4 * kWarps));
+        switch (k) {
+            case 4: k_block_argmin_i32_grp<1><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            case 8: k_block_argmin_i32_grp<2><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            case 16: k_block_argmin_i32_grp<4><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            case 32: k_block_argmin_i32_grp<8><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            case 64: k_block_argmin_i32_grp<16><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            default: k_block_argmin_i32_grp<32><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+        }
+        if (nblk > nfull)  // the clipped trailing block
+            k_block_argmin_i32_gen<<<1, kThreads, 0, stream>>>(A, n, k, nfull, nblk, keys);
+        return nblk > nfull ? 2 : 1;
+    }
+    if (k < 32) {
+        k_block_argmin_i32_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(A, n, k, nblk,
+                                                                                                  keys);
+    } else if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
         k_block_argmin_i32_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys);
     } else {
         k_block_argmin_i32_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, k, 0, nblk, keys);
@@ -147,6 +235,12 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
 int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t* len_dev,
                              uint32_t k, uint64_t* keys, uint64_t* b_dev, cudaStream_t stream) {
     uint64_t nblk = (len_max + k - 1) / k;
+    if (k < 32 && !len_dev && !b_dev) {  // host-known length (multi-level chains)
+        if (nblk == 0) return 0;
+        k_block_argmin_keys_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+            K, len_max, k, nblk, keys);
+        return 1;
+    }
     if (nblk == 0) nblk = 1;  // still publish *b_dev
     k_block_argmin_keys<<<grid_for_warps(nblk), kThreads, 0, stream>>>(K, len_max, len_dev, k, keys,
                                                                        b_dev);
@@ -292,6 +386,12 @@ int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint6
                                 uint32_t k, uint64_t* keys, uint64_t* sub, uint64_t* b_dev,
                                 cudaStream_t stream) {
     uint64_t nblk = (len_max + k - 1) / k;
+    if (k < 32 && !len_dev && !b_dev) {  // host-known length (multi-level chains)
+        if (nblk == 0) return 0;
+        k_block_argmin_keys_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+            K, len_max, k, nblk, keys);
+        return 1;
+    }
     if (nblk == 0) nblk = 1;  // still publish *b_dev
     // few blocks (A_Q of a small batch): one warp per CTA spreads them over all SMs
     const unsigned nt = nblk <= uint64_t(148) * 32 ? 32u : unsigned(kThreads);

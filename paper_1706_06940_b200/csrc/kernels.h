@@ -76,6 +76,14 @@ int launch_query_contracted(const uint64_t* AQ, const uint64_t* aq_len_dev, uint
                             uint64_t* answers, cudaStream_t stream,
                     const CtlPublish& pub = CtlPublish{});
 
+// ---------------------------------------------------------------- query_chain.cu
+// Multi-level BbST for any dividing chain ks[0] < ... < ks[h-1] (2 <= h <= kMaxChain):
+// M[j] = ks[j]-block minima keys (j < h - 1), ST over the ks[h-1]-blocks.
+constexpr uint32_t kMaxChain = 8;
+int launch_query_chain(const int32_t* A, uint64_t n, const uint32_t* ks, uint32_t h,
+                       const uint64_t* const* M, const uint64_t* ST, uint64_t stride,
+                       const uint64_t* Q, uint64_t q, uint64_t* answers, uint32_t* err,
+                       cudaStream_t stream, const CtlPublish& pub);
 // ---------------------------------------------------------------- radix_sort.cu
 size_t radix_sort_temp_bytes(uint64_t m, int bits);     // zeroed scratch (histograms, tickets)
 size_t radix_sort_status_words(uint64_t m, int bits);   // epoch-tagged look-back words

@@ -158,7 +158,7 @@ def test_multilevel_configs(engine, orc):
         for k in (64, 256, 512):
             for sk in (SortKind.Bitmap, SortKind.Radix):
                 assert np.array_equal(engine.solve_batch_bbst_con(A4, Q4, k, sk), want4), (kind, k, sk)
-    for bad in [(16, 512), (32, 48), (32, 16), (64, 512), (32, 64, 512)]:
+    for bad in [(32, 48), (32, 16), (7, 7), (0, 4), (2, 4, 6), tuple(2 ** i for i in range(1, 10))]:
         with pytest.raises(InvalidArgument):
             engine.solve_batch_bbst_ml(A, Q, bad)
     # unaligned device pointer (scalar fallbacks)
@@ -167,6 +167,39 @@ def test_multilevel_configs(engine, orc):
     dQ = torch.from_numpy(Q.view(np.int64)).cuda()
     assert np.array_equal(engine.solve_batch_bbst_ml(dA, dQ, (32, 512)).cpu().numpy().view(np.uint64), want)
     assert np.array_equal(engine.solve_batch_bbst(dA, dQ, 512).cpu().numpy().view(np.uint64), want)
+
+
+def test_multilevel_general_chains(engine, orc):
+    """SPEC.md:313: oracle equality for cfg in {[1],[2],[7],[k],[k1,k2],[k1,k2,k3]}
+    with randomized dividing chains, n <= 1e5 (query_chain.cu for every chain
+    other than [k] and [32, k])."""
+    A = np.array([5, 3, 8, 2, 7, 6, 9, 1], np.int32)  # SPEC.md:287-298 worked instance
+    assert list(engine.solve_batch_bbst_ml(A, np.array([[0, 7]], np.uint64), (2, 4))) == [7]
+    assert list(engine.solve_batch_bbst_ml(A, np.array([[1, 4], [3, 6]], np.uint64), (2, 4))) == [3, 3]
+    r = np.random.default_rng(2024)
+    fixed = [(1, 2), (2, 4), (1, 4, 64), (2, 4, 8), (3, 6, 24), (7, 14), (16, 512), (64, 512),
+             (32, 64, 512), (4, 16, 64, 256, 1024), (1, 2, 4, 8, 16, 32, 64, 128), (5, 25, 125, 625)]
+    chains = list(fixed)
+    for _ in range(10):  # randomized dividing chains
+        h = int(r.integers(2, 5))
+        ks = [int(r.integers(1, 9))]
+        for _ in range(h - 1):
+            ks.append(ks[-1] * int(r.integers(2, 6)))
+        chains.append(tuple(ks))
+    for trial, ks in enumerate(chains):
+        n = int(r.integers(1, 100_000))
+        vkind = ["uniform", "ties16", "walk", "binary"][trial % 4]
+        qk = ["uniform", "short", "mixed", "degenerate"][trial % 4]
+        A = _values(r, n, vkind)
+        Q = _queries(r, n, int(r.integers(1, 5000)), qk)
+        got = engine.solve_batch_bbst_ml(A, Q, ks)
+        want = orc.naive_numpy(A, Q)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (ks, n, vkind, qk, bad[:5], got[bad[:5]], want[bad[:5]])
+    # range errors and empty batches behave as on the other paths
+    with pytest.raises(Exception):
+        engine.solve_batch_bbst_ml(A, np.array([[0, A.shape[0]]], np.uint64), (2, 4))
+    assert engine.solve_batch_bbst_ml(A, np.zeros((0, 2), np.uint64), (2, 4)).shape[0] == 0
 
 
 def test_device_pointers(engine, orc):
@@ -278,7 +311,7 @@ def test_stage_contract_errors(engine):
         engine.remap_queries(make_queries([3], [5]), bad)
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 32, 512])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8, 16, 32, 64, 128, 512])
 def test_stage_block_sparse(engine, orc, k):
     import ctypes as C
     r = np.random.default_rng(k)
