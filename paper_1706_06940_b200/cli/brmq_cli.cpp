@@ -3,7 +3,7 @@
 //   brmq gen-array   --n N --seed S --out F [--kind permutation|uniform|ties16|walk]
 //   brmq gen-queries --n N --q Q --seed S --out F [--kind uniform|loguniform|mixed]
 //   brmq run --algo {naive|sparse|st-rmq-con|bbst-con|bbst|bbst-ml} --array F --queries F
-//            [--k K | --chain K1,K2] [--runs R=7] [--threads T=1] [--sort radix|comparison|bitmap]
+//            [--k K | --chain K1,K2,...] [--runs R=7] [--threads T=1] [--sort radix|comparison|bitmap]
 //            --csv F [--plot F] [--answers F]
 //   brmq verify --array F --queries F --answers F [--threads T]
 //
@@ -80,7 +80,7 @@ int usage() {
             "usage: brmq gen-array --n N --seed S --out F [--kind permutation|uniform|ties16|walk]\n"
             "       brmq gen-queries --n N --q Q --seed S --out F [--kind uniform|loguniform|mixed]\n"
             "       brmq run --algo {naive|sparse|st-rmq-con|bbst-con|bbst|bbst-ml} --array F\n"
-            "                --queries F [--k K | --chain K1,K2] [--runs R] [--threads T]\n"
+            "                --queries F [--k K | --chain K1,K2,...] [--runs R] [--threads T]\n"
             "                [--sort radix|comparison|bitmap] --csv F [--plot F] [--answers F]\n"
             "       brmq verify --array F --queries F --answers F [--threads T]\n");
     return 1;
