@@ -220,6 +220,55 @@ __device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t 
     run = pack_key(rv, p0 + ri);
 }
 
+// row_pass_all without branches per element: the closing key of a boundary at
+// j is m = leftmost-min(run state, (v_j, j)) -- the update a non-boundary
+// element makes anyway -- so every element costs min / compare / select, and a
+// boundary additionally captures m into the lane's shared-memory slots
+// (predicated store, no branch) and restarts the run at (v_j, j).  The captures
+// are emitted afterwards: capture 0 is the row's head part, capture i >= 1 closes
+// area rank + i - 1.  Needs popc(fl) <= kCap (the caller checks; row_pass_all
+// otherwise).  c5-con: the branchy per-element walk was ~15 instructions per
+// element (BSSY/BRA/BSYNC around every compare), this one 8.
+constexpr int kCap = 16;  // capture slots per lane
+constexpr size_t kCapSmem = size_t(NW) * kCap * 32 * 8;  // dynamic shared memory of k_contract
+template <bool MARKED, class RW>
+__device__ __forceinline__ void row_pass_cap(const RW& rw, uint32_t r, uint32_t fl, uint64_t rank,
+                                             uint64_t* __restrict__ aq, uint64_t& hp, uint64_t& run,
+                                             uint32_t cap /* shared address of slot 0 of this lane */) {
+    const uint32_t p0 = uint32_t(rw.pos(r, 0));
+    int32_t rv = 0x7FFFFFFF;
+    uint32_t ri = 0;
+    uint32_t at = cap;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int4 x = rw.chunk(r, c);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t j = uint32_t(4 * c + e);
+            const int32_t v = comp(x, e);
+            const bool lt = v < rv;  // strict: the earlier position keeps ties
+            const int32_t mv = lt ? v : rv;
+            const uint32_t mi = lt ? j : ri;
+            const bool isb = (fl >> j) & 1u;
+            if (isb) {  // predicated (no divergent branch): capture, advance, restart
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(at), "r"(uint32_t(mv)), "r"(mi) : "memory");
+                at += 32u * 8u;
+            }
+            rv = isb ? v : mv;
+            ri = isb ? j : mi;
+        }
+    }
+    run = pack_key(rv, p0 + ri);
+    const uint32_t nb = __popc(fl);
+    for (uint32_t i = 0; i < nb; ++i) {
+        uint32_t cv, ci;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cv), "=r"(ci) : "r"(cap + i * 32u * 8u) : "memory");
+        const uint64_t k = pack_key(int32_t(cv), p0 + ci);
+        if (i == 0) hp = k;
+        else aq[aq_slot<MARKED>(rank + i - 1)] = k;
+    }
+}
+
 // Warp `warp`'s piece of CTA `cta`'s range: warp tiles [wa, wa + cnt) of range
 // cta (R tiles), clipped to the span [b0, blast]; cnt = 0 when empty.  Shared by
 // the contraction and the piece-count kernel, so both cut identically.
@@ -304,6 +353,7 @@ struct ContractArgs {
 template <bool VEC, bool MARKED, bool SPARSE = true>
 __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
     __shared__ __align__(128) int4 s_rows[NW][kWTile / 4];  // per warp: 32 rows x 128 B, swizzled
+    extern __shared__ __align__(16) uint2 s_cap[];  // [NW][kCap][32] boundary captures (dense rows)
     __shared__ uint32_t s_cnt[NW];
     __shared__ uint64_t s_tail[NW];
     __shared__ uint32_t s_has[NW];
@@ -497,7 +547,13 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
             wc = __shfl_sync(kFull, cinc, 31);
             const uint64_t rank = rank_run + (cinc - cntb);
             uint64_t hp = kNoKey;
-            if (!GEN) row_pass_all<MARKED>(rs, lane, fl, rank, c.aq, hp, run);
+            if (!GEN) {
+                if (!__any_sync(kFull, __popc(fl) > kCap))
+                    row_pass_cap<MARKED>(rs, lane, fl, rank, c.aq, hp, run,
+                                         smem_u32(s_cap) + (warp * kCap * 32u + lane) * 8u);
+                else
+                    row_pass_all<MARKED>(rs, lane, fl, rank, c.aq, hp, run);
+            }
             else if (any && fl) row_pass<MARKED>(rs, lane, fl, jlo, jhi, rank, c.aq, hp, run);
             SegMin inc{run, cntb != 0};
 #pragma unroll
@@ -647,8 +703,10 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
             bool has = false;
             const bool live = j >= int64_t(cfirst);  // CTAs before b0's hold nothing
             if (live) {
-                while (status_state(sw = ld_relaxed_u64(c.st_part + j), epoch) == kStInvalid) {
-                }
+                // backoff: a spinning warp would take issue slots from the warps of
+                // its SM still streaming (c5-con: 4.1M polls per solve without it)
+                while (status_state(sw = ld_relaxed_u64(c.st_part + j), epoch) == kStInvalid)
+                    __nanosleep(256);
                 has = status_flag(sw);
             }
             __threadfence();  // acquire: the tails were stored before their descriptors
@@ -664,13 +722,25 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
 }
 
 int contract_grid() {
-    static int grid = 0;
+    // per device: the shared-memory attribute belongs to the device's context
+    // (the grid is the same on identical parts, kept per device anyway)
+    static int grids[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& grid = grids[dev & 63];
     if (grid == 0) {
-        int dev = 0, sms = 0, per_v = 0, per_s = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per_v = 0, per_s = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_v, k_contract<true, false>, NT, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, k_contract<false, true>, NT, 0);
+        const void* fns[] = {reinterpret_cast<const void*>(k_contract<true, false>),
+                             reinterpret_cast<const void*>(k_contract<true, false, false>),
+                             reinterpret_cast<const void*>(k_contract<true, true>),
+                             reinterpret_cast<const void*>(k_contract<true, true, false>),
+                             reinterpret_cast<const void*>(k_contract<false, false>),
+                             reinterpret_cast<const void*>(k_contract<false, true>)};
+        for (const void* f : fns)  // the capture slots take the block past 48 KB of shared memory
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCapSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_v, k_contract<true, false>, NT, kCapSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_s, k_contract<false, true>, NT, kCapSmem);
         int per = per_v < per_s ? per_v : per_s;
         if (per < 1) per = 1;
         grid = sms * per;
@@ -726,8 +796,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                                             : reinterpret_cast<const void*>(k_contract<true, false>)))
                          : (marked ? reinterpret_cast<const void*>(k_contract<false, true>)
                                    : reinterpret_cast<const void*>(k_contract<false, false>));
-    cudaLaunchCooperativeKernel(fn,
-                                dim3(G), dim3(NT), params, 0, s);
+    cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), params, kCapSmem, s);
     return 1;  // launch errors surface through the caller's cudaGetLastError
 }
 
