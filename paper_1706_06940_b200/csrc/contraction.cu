@@ -58,7 +58,7 @@ constexpr int kWTile = 32 * kRow;   // 1024 positions = 4 KB per warp tile
 constexpr int kTile = 4 * kWTile;   // 4096: the partition unit
 static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
 #ifndef BRMQ_KDENSE
-#define BRMQ_KDENSE 4
+#define BRMQ_KDENSE 2
 #endif
 #ifndef BRMQ_CONTRACT_MINB
 #define BRMQ_CONTRACT_MINB 2  // 2 CTAs per SM: <= 128 registers (129 would halve the residency)
