@@ -50,7 +50,7 @@
 namespace brmq {
 namespace {
 
-constexpr int NW = 8;               // warps per CTA, one stream each (2 CTAs per SM at 128 registers)
+constexpr int NW = int(kContractWarps);  // warps per CTA, one stream each (2 CTAs per SM at 128 registers)
 static_assert(NW == int(kContractWarps), "piece layout shared with the endpoint stage");
 constexpr int NT = NW * 32;
 constexpr int kRow = 32;            // positions per lane = one 128-byte row

@@ -109,7 +109,10 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
 // Boundaries per contraction piece (pcnt[g * 8 + w], 8 warps per range) and per
 // range (rcnt[g]), popcounted from the bitmap.
-constexpr uint32_t kContractWarps = 8;
+#ifndef BRMQ_CWARPS
+#define BRMQ_CWARPS 8
+#endif
+constexpr uint32_t kContractWarps = BRMQ_CWARPS;
 int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* pcnt,
                        uint32_t* rcnt, cudaStream_t s);
 size_t unique_status_words(uint64_t m);
