@@ -82,3 +82,13 @@ def test_run_all_algorithms(cli, tmp_path):
     by = {row["algo"]: row for row in rows}
     assert int(by["bbst-con"]["extra_bytes"]) == H.account_memory("bbst-con", n, q, (512,))[0]
     assert float(by["bbst-con"]["t_sort_ns"]) > 0 and float(by["bbst-con"]["t_contract_ns"]) > 0
+    # a three-level chain through the CLI (query_chain.cu), recorded as k_chain "8;64;512"
+    r = tmp_path / "ml3.rmqr"
+    p = _run(cli, "run", "--algo", "bbst-ml", "--array", a, "--queries", qf, "--chain", "8,64,512",
+             "--runs", 1, "--csv", table, "--answers", r)
+    assert p.returncode == 0, p.stderr
+    assert np.array_equal(H.read_answers(r), want)
+    assert list(csv.DictReader(open(table)))[-1]["k_chain"] == "8;64;512"
+    p = _run(cli, "run", "--algo", "bbst-ml", "--array", a, "--queries", qf, "--chain", "8,60",
+             "--runs", 1, "--csv", table)
+    assert p.returncode != 0  # not a dividing chain
