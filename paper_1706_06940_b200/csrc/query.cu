@@ -34,6 +34,14 @@ namespace brmq {
 namespace {
 
 constexpr int kThreads = 256;
+// k_query's register budget for the k = 512 batch instance (4 vectors per lane): 40
+// resident warps per SM (<= 48 registers; the other instances would spill).  The
+// unconstrained build took 64 registers (32 warps); c3 / c4 / c5 query phases
+// 0.906 / 0.271 / 0.268 -> 0.875 / 0.261 / 0.247 ms (48 warps at 40 registers
+// spilled and lost: 0.920 / 0.300 / 0.251).
+#ifndef BRMQ_QUERY_WARPS
+#define BRMQ_QUERY_WARPS 40
+#endif
 
 struct ElemI32 {
     using vec_t = int4;
@@ -186,7 +194,7 @@ __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64
 // WPQ: one warp per query (small batches: the per-warp rounds of partial scans
 // are the latency chain, so spread the queries over 32x more warps).
 template <class E, class QP, int VPL, int TPR, bool WPQ = false, int NT = kThreads>
-__global__ void __launch_bounds__(NT) k_query(E elem, QP qp, uint32_t k_rt,
+__global__ void __launch_bounds__(NT, (VPL == 4 && TPR == 1 && !WPQ ? BRMQ_QUERY_WARPS / (NT / 32) : 1)) k_query(E elem, QP qp, uint32_t k_rt,
                                               const uint64_t* __restrict__ ST,
                                               uint64_t stride, uint64_t q,
                                               uint64_t* __restrict__ answers,
