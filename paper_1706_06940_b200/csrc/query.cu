@@ -39,6 +39,14 @@ constexpr int kThreads = 256;
 // unconstrained build took 64 registers (32 warps); c3 / c4 / c5 query phases
 // 0.906 / 0.271 / 0.268 -> 0.875 / 0.261 / 0.247 ms (48 warps at 40 registers
 // spilled and lost: 0.920 / 0.300 / 0.251).
+// k_query_flat's register budget: the 128-thread instances for 56 resident warps
+// per SM (32 registers, a few spilled words), the 32-thread (small-batch)
+// instances for 64 registers as before.  c3 [32, 512] query 0.471 -> 0.428 ms, c3-con
+// 0.533 -> 0.486 ms, c5-con 0.411 -> 0.405 ms (48 warps: 0.442 / 0.505 / 0.407).
+// (An explicit minimum of 1 CTA lets ptxas take up to 255 registers: 0.90 ms.)
+#ifndef BRMQ_FLAT_WARPS
+#define BRMQ_FLAT_WARPS 56
+#endif
 #ifndef BRMQ_QUERY_WARPS
 #define BRMQ_QUERY_WARPS 40
 #endif
@@ -194,7 +202,7 @@ __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64
 // WPQ: one warp per query (small batches: the per-warp rounds of partial scans
 // are the latency chain, so spread the queries over 32x more warps).
 template <class E, class QP, int VPL, int TPR, bool WPQ = false, int NT = kThreads>
-__global__ void __launch_bounds__(NT, (VPL == 4 && TPR == 1 && !WPQ ? BRMQ_QUERY_WARPS / (NT / 32) : 1)) k_query(E elem, QP qp, uint32_t k_rt,
+__device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
                                               const uint64_t* __restrict__ ST,
                                               uint64_t stride, uint64_t q,
                                               uint64_t* __restrict__ answers,
@@ -301,6 +309,22 @@ __global__ void __launch_bounds__(NT, (VPL == 4 && TPR == 1 && !WPQ ? BRMQ_QUERY
     publish_control(pub);
 }
 
+template <class E, class QP, int VPL, int TPR, bool WPQ = false, int NT = kThreads>
+__global__ void __launch_bounds__(NT) k_query(E elem, QP qp, uint32_t k_rt, const uint64_t* __restrict__ ST,
+                                              uint64_t stride, uint64_t q, uint64_t* __restrict__ answers,
+                                              const CtlPublish pub) {
+    query_body<E, QP, VPL, TPR, WPQ, NT>(elem, qp, k_rt, ST, stride, q, answers, pub);
+}
+// the k = 512 batch instance with its register budget (BRMQ_QUERY_WARPS)
+template <class E, class QP, int VPL, int TPR>
+__global__ void __launch_bounds__(128, BRMQ_QUERY_WARPS / 4) k_query_budget(E elem, QP qp, uint32_t k_rt,
+                                                                            const uint64_t* __restrict__ ST,
+                                                                            uint64_t stride, uint64_t q,
+                                                                            uint64_t* __restrict__ answers,
+                                                                            const CtlPublish pub) {
+    query_body<E, QP, VPL, TPR, false, 128>(elem, qp, k_rt, ST, stride, q, answers, pub);
+}
+
 constexpr uint64_t kWarpPerQueryMax = 16384;  // batches up to this size: one warp per query
 
 template <class E, class QP, int VPL, int TPR>
@@ -313,6 +337,11 @@ void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint6
     }
     // 128-thread CTAs: a CTA holds its SM slot until its slowest warp is done
     // (c3 h = 1: 256 -> 128 threads 1.15 -> 1.04 ms; 64 is slower on c5)
+    if constexpr (VPL == 4 && TPR == 1) {
+        k_query_budget<E, QP, VPL, TPR><<<unsigned((q + 127) / 128), 128, 0, s>>>(e, qp, k, ST, stride, q,
+                                                                                 ans, pub);
+        return;
+    }
     k_query<E, QP, VPL, TPR, false, 128><<<unsigned((q + 127) / 128), 128, 0, s>>>(e, qp, k, ST, stride,
                                                                                   q, ans, pub);
 }
@@ -771,7 +800,7 @@ __device__ __forceinline__ void ml_flat_group(const E& elem, const QP& qp, uint3
 }
 
 template <class E, class QP, int NT>
-__global__ void __launch_bounds__(NT) k_query_flat(const E elem, const QP qp, uint32_t kshift,
+__global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 2048 / NT)) k_query_flat(const E elem, const QP qp, uint32_t kshift,
                                                    const uint64_t* __restrict__ ST, uint64_t stride,
                                                    const uint64_t* __restrict__ sub, uint64_t q,
                                                    uint64_t* __restrict__ answers,

@@ -9,6 +9,7 @@ from paper_1706_06940_b200 import Engine
 
 ap = argparse.ArgumentParser()
 ap.add_argument('--config', default='c3')
+ap.add_argument('--chains', default='')
 a = ap.parse_args()
 A, Q = gen_workload(a.config)
 eng = Engine(0)
@@ -17,7 +18,7 @@ dA = torch.from_numpy(A).cuda(); dQ = torch.from_numpy(Q.view(np.int64)).cuda()
 dO = torch.empty(Q.shape[0], dtype=torch.int64, device='cuda')
 flush = L2Flush(torch, 'cuda')
 ref = None
-for ks in [(512,), (32, 512), (64, 512), (16, 512), (128, 4096), (8, 64, 512), (4, 32, 512), (32, 256, 4096)]:
+for ks in ([tuple(int(v) for v in x.split(',')) for x in a.chains.split(';')] if a.chains else [(512,), (32, 512), (64, 512), (16, 512), (128, 4096), (8, 64, 512), (4, 32, 512), (32, 256, 4096)]):
     f = lambda: eng.solve_batch_bbst_ml(dA, dQ, ks, out=dO)
     ms, st, _ = time_solves(eng, torch, s, f, 5, 3, flush, timing=1)
     got = dO.cpu().numpy()
