@@ -66,11 +66,21 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "src": "fallback"}
 
 
-def gen_workload(name: str, n: int | None = None, q: int | None = None):
-    from paper_1706_06940_b200 import _lib
+def gen_workload(name: str, n: int | None = None, q: int | None = None, L=None):
+    """The seeded workload of config `name` (include/brmq_workload.h).  L is the
+    library exporting brmq_workload_*: libbrmq.so by default; the reference arm
+    passes oracle/_ref/libbrmq_ref.so (the same generator source compiled into the
+    reference build, oracle/Makefile) so that its process never loads libbrmq.so."""
     ak, n0, qk, q0, c, _, _ = CONFIGS[name]
     n, q = n or n0, q or q0
-    L = _lib.lib()
+    if L is None:
+        from paper_1706_06940_b200 import _lib
+        L = _lib.lib()
+    for f in (L.brmq_workload_array, L.brmq_workload_queries):
+        f.restype = C.c_int
+    L.brmq_workload_array.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint]
+    L.brmq_workload_queries.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
+                                        C.c_uint]
     A = np.empty(n, np.int32)
     Q = np.empty((q, 2), np.uint64)
     assert L.brmq_workload_array(ak, n, SEED0 + c, A.ctypes.data, 0) == 0
@@ -128,10 +138,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ reference arm
+def loaded_libraries() -> list[str]:
+    """Shared objects mapped into this process (Linux /proc/self/maps)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ".so" in ln.split()[-1]})
+    except OSError:
+        return []
+
+
 def run_reference(args) -> dict:
     import oracle
     name = args.config
-    A, Q = gen_workload(name)
+    A, Q = gen_workload(name, L=oracle.ref())
+    own = [p for p in loaded_libraries() if p.endswith("libbrmq.so")]
+    assert not own, f"reference arm must not load the engine library: {own}"
     q = Q.shape[0]
     th = oracle.nthreads()
     L = oracle.ref()
@@ -151,7 +172,9 @@ def run_reference(args) -> dict:
         "impl": "reference", "metric": metric_name(), "value": v, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": config_dict(name, "reference_cpu"),
+        "data": "synthetic", "config": config_dict(name),
+        "variant": "reference CPU pipeline: collect -> radix sort -> build_contracted -> remap "
+                   "-> ElementSparseTable",
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": th, "kind": "reference",
                          "sample": f"full {name} workload per step (reference sources compiled "
                                    f"unmodified, build_contracted threads={th})",
@@ -179,9 +202,11 @@ def metric_name() -> str:
     return "batched RMQ queries/s incl. preprocess (n=1e8 int32); scan GB/s vs HBM peak"
 
 
-def config_dict(name: str, variant: str) -> dict:
+def config_dict(name: str) -> dict:
+    """The workload, identical in both arms (the algorithm each arm runs is the
+    line's top-level "variant")."""
     ak, n, qk, q, c, _, desc = CONFIGS[name]
-    return {"workload": f"{name}: {desc}", "n": n, "q": q, "k": 512, "variant": variant,
+    return {"workload": f"{name}: {desc}", "n": n, "q": q, "k": 512,
             "seed": SEED0 + c, "l2": "flushed before every step, outside the timed window: 256 MiB write, then a 256 MiB read (the write's dirty lines drain before the window)",
             "parallelism": "replicas (one independent solve per GPU)"}
 
@@ -370,7 +395,7 @@ def run_ours(args) -> dict:
         "metric": metric_name(), "value": aggregate_value(q, world, t_step), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": config_dict(name, variant),
+        "data": "synthetic", "config": config_dict(name), "variant": variant,
         "e2e": {"value": aggregate_value(q, world, e2e_t), "unit": "queries/s",
                 "h2d_bytes_per_step": nbytes_a + nbytes_q, "d2h_bytes_per_step": nbytes_o,
                 "ms_per_step": e2e_t},

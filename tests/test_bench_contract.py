@@ -37,3 +37,18 @@ def test_reference_arm_other_ranks_silent():
     p = _run("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "0",
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+def test_reference_arm_never_loads_engine():
+    """The reference arm builds its workload with the generator compiled into
+    oracle/_ref (oracle/Makefile), so libbrmq.so is never mapped in its process."""
+    code = ("import sys, bench, oracle; sys.argv=['bench.py']; "
+            "A, Q = bench.gen_workload('c1', L=oracle.ref()); "
+            "assert not [p for p in bench.loaded_libraries() if p.endswith('libbrmq.so')]; "
+            "from paper_1706_06940_b200 import _lib; _lib.lib(); "
+            "B, R = bench.gen_workload('c1'); "
+            "assert (A == B).all() and (Q == R).all(); "
+            "assert [p for p in bench.loaded_libraries() if p.endswith('libbrmq.so')]; print('ok')")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                       timeout=300)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
