@@ -247,9 +247,11 @@ class L2Flush:
         self.torch.max(self.r)
 
 
-def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2):
+def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2, poison=None):
     """Per-step CUDA-event windows on the library stream; L2 flushed between steps.
-    timing: library stage events (0 off, 1 every stage, 2 only the roofline kernel)."""
+    timing: library stage events (0 off, 1 every stage, 2 only the roofline kernel).
+    poison: called before every step, outside the window (fills the answer buffer
+    with 0xFF so a replay that wrote nothing cannot pass the check that follows)."""
     eng.set_timing(timing)
     for _ in range(warmup):
         flush()
@@ -257,6 +259,8 @@ def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2):
     torch.cuda.synchronize()
     ms, stage_acc, launches = [], {}, 0
     for _ in range(steps):
+        if poison is not None:
+            poison()
         flush()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
@@ -326,19 +330,33 @@ def run_ours(args) -> dict:
     # node costs ~5-7 us of serialisation each on this part, measured with
     # tools/timing_modes.py).  The roofline kernel is then timed by CUDA events
     # around it in a second K-step pass of the same workload (timing level 2).
+    poison = lambda: dAns.fill_(-1)  # noqa: E731
+
+    def check(tag, buf=None):
+        if want is None:
+            return None
+        got = (dAns if buf is None else buf).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), f"{tag}: answers of the last replay differ from the oracle"
+        return True
+
     with Clocks(local) as clk:
         ms, _, launches = time_solves(eng, torch, stream, solve, args.steps, args.warmup, flush,
-                                      timing=0)
-        ms_roof, stages, _ = time_solves(eng, torch, stream, solve, args.steps, 1, flush, timing=2)
+                                      timing=0, poison=poison)
+        checks = {"timed": check("timed region")}
+        ms_roof, stages, _ = time_solves(eng, torch, stream, solve, args.steps, 1, flush, timing=2,
+                                         poison=poison)
+        checks["roofline_pass"] = check("roofline pass")
     torch.cuda.synchronize()
     # per-stage breakdown (every stage bracketed by events; informative, not the headline)
-    _, breakdown, _ = time_solves(eng, torch, stream, solve, 5, 1, flush, timing=1)
+    _, breakdown, _ = time_solves(eng, torch, stream, solve, 5, 1, flush, timing=1, poison=poison)
+    checks["stage_pass"] = check("per-stage pass")
     # the other endpoint-sort pipeline on the same workload (same answers)
     variants = {variant: aggregate_value(q, 1, statistics.mean(ms))}
     if variant != "bbst":
         alt = "con_bitmap" if variant == "con_radix" else "con_radix"
         ms_alt, _, _ = time_solves(eng, torch, stream, lambda: solve(v=alt), args.steps, 2, flush,
-                                   timing=0)
+                                   timing=0, poison=poison)
+        checks[alt] = check(alt)
         variants[alt] = aggregate_value(q, 1, statistics.mean(ms_alt))
     t_step = max_over_ranks(statistics.mean(ms), dist, dev)
     if dist:
@@ -364,10 +382,11 @@ def run_ours(args) -> dict:
             eng.solve_batch_bbst_con(hA, hQ, 512, VARIANT_SORT[variant], out=hO)
 
     e2e_ms, _, _ = time_solves(eng, torch, stream, solve_host, max(3, args.steps // 2), 2, flush,
-                               timing=0)
+                               timing=0, poison=lambda: hO.fill(np.uint64(0xFFFFFFFFFFFFFFFF)))
     e2e_t = statistics.mean(e2e_ms)
     if want is not None:
         assert np.array_equal(hO, want), "e2e answers differ from the reference oracle"
+        checks["e2e"] = True
     L.brmq_host_free(hp)
     e2e_t = max_over_ranks(e2e_t, dist, dev)
 
@@ -413,6 +432,7 @@ def run_ours(args) -> dict:
         "stages_ms": {k: round(v[0], 5) for k, v in breakdown.items()},
         "dominant_stage": dom,
         "variants_queries_per_s": variants,
+        "bit_exact_vs_reference": checks,
         "clocks": clk.summary(),
         "info": info,
     }
@@ -437,8 +457,11 @@ def run_ours(args) -> dict:
 
 
 def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
-    """North-star sweep: end-to-end queries/s at n = 1e8 for q = 1e3 .. 1e7, both variants
-    (device-resident inputs; each point checked against the oracle where cheap)."""
+    """North-star sweep: end-to-end queries/s at n = 1e8 for q = 1e3 .. 1e7, every
+    variant (device-resident inputs).  The answer buffer is poisoned before every
+    step and the last replay of each point is checked against the reference
+    pipeline (oracle/_ref) on the host."""
+    import oracle
     from paper_1706_06940_b200 import _lib
     L = _lib.lib()
     n = A.shape[0]
@@ -446,6 +469,7 @@ def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
     for q in (1_000, 10_000, 100_000, 1_000_000, 10_000_000):
         Q = np.empty((q, 2), np.uint64)
         L.brmq_workload_queries(0, n, q, SEED0 + 2, Q.ctypes.data, 0)
+        want = None if args.no_cpu else oracle.solve_oracle(A, Q)
         dQ = torch.from_numpy(Q.view(np.int64)).to(dA.device)
         dO = torch.empty(q, dtype=torch.int64, device=dA.device)
         for v in ("con_radix", "con_bitmap", "bbst", "st_rmq_con"):
@@ -456,10 +480,13 @@ def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
                     eng.solve_batch_st_rmq_con(dA, dQ, out=dO)
                 else:
                     eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[v], out=dO)
-            ms, _, _ = time_solves(eng, torch, stream, f, 5, 2, flush, timing=0)
+            pz = lambda: dO.fill_(-1)  # noqa: E731
+            ms, _, _ = time_solves(eng, torch, stream, f, 5, 2, flush, timing=0, poison=pz)
+            ok = None if want is None else bool(np.array_equal(dO.cpu().numpy().view(np.uint64), want))
             _, stages, _ = time_solves(eng, torch, stream, f, 2, 0, flush, timing=1)
             t = statistics.mean(ms)
             out.append({"q": q, "variant": v, "queries_per_s": q / (t * 1e-3), "ms": t,
+                        "bit_exact_vs_reference": ok,
                         "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}})
     return out
 
@@ -489,9 +516,10 @@ def run_configs(eng, torch, stream, flush, args) -> dict:
             "st_rmq_con": lambda: eng.solve_batch_st_rmq_con(dA, dQ, out=dO),
         }
         for v, f in variants.items():
-            ms, _, _ = time_solves(eng, torch, stream, f, 5, 3, flush, timing=0)
-            _, stages, _ = time_solves(eng, torch, stream, f, 2, 0, flush, timing=1)
+            pz = lambda: dO.fill_(-1)  # noqa: E731
+            ms, _, _ = time_solves(eng, torch, stream, f, 5, 3, flush, timing=0, poison=pz)
             ok = None if want is None else bool(np.array_equal(dO.cpu().numpy().view(np.uint64), want))
+            _, stages, _ = time_solves(eng, torch, stream, f, 2, 0, flush, timing=1)
             t = statistics.mean(ms)
             res[v] = {"queries_per_s": q / (t * 1e-3), "ms": t, "bit_exact_vs_reference": ok,
                       "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}}

@@ -221,6 +221,88 @@ def test_device_pointers(engine, orc):
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), variant
 
 
+def _solve_into(engine, variant, dA, dQ, out):
+    if variant == "bbst":
+        return engine.solve_batch_bbst(dA, dQ, 512, out=out)
+    if variant == "bbst_ml":
+        return engine.solve_batch_bbst_ml(dA, dQ, (32, 512), out=out)
+    if variant == "bbst_ml3":
+        return engine.solve_batch_bbst_ml(dA, dQ, (8, 64, 512), out=out)
+    if variant == "st_rmq_con":
+        return engine.solve_batch_st_rmq_con(dA, dQ, out=out)
+    kind = SortKind.Radix if variant == "con_radix" else SortKind.Bitmap
+    return engine.solve_batch_bbst_con(dA, dQ, 512, kind, out=out)
+
+
+def test_graph_replays_poisoned(engine, orc):
+    """Device-pointer solves are captured once into a CUDA graph and replayed
+    (api.cu run_solve): every replay must rewrite every answer.  The output is
+    filled with 0xFF before each call, shapes and q are interleaved so that the
+    look-back epochs, the persistent bitmap and the control header are reused
+    across graphs, and every replay is checked (naive.hpp:13-21, leftmost)."""
+    torch = pytest.importorskip("torch")
+    r = np.random.default_rng(31)
+    cases = []
+    for n, q, vk, qk in ((300_000, 40_000, "ties16", "mixed"), (1_000_003, 100_000, "uniform", "uniform"),
+                         (70_001, 5_000, "walk", "short"), (1_000_003, 7, "binary", "uniform")):
+        A = _values(r, n, vk)
+        Q = _queries(r, n, q, qk)
+        cases.append((torch.from_numpy(A).cuda(), torch.from_numpy(Q.view(np.int64)).cuda(),
+                      torch.empty(q, dtype=torch.int64, device="cuda"), orc.solve_oracle(A, Q)))
+    variants = VARIANTS + ["bbst_ml3"]
+    for rep in range(3):
+        for ci, (dA, dQ, out, want) in enumerate(cases):
+            for variant in variants:
+                out.fill_(-1)
+                _solve_into(engine, variant, dA, dQ, out)
+                got = out.cpu().numpy().view(np.uint64)
+                bad = np.nonzero(got != want)[0]
+                assert bad.size == 0, (rep, ci, variant, bad[:5])
+
+
+@pytest.mark.slow
+def test_positions_above_2_31(engine, orc):
+    """n = 2^31 + 4099 (the reference allows n up to 2^32 - 1,
+    element_sparse_table.cpp:12-13; Endpoint.pos is uint32, contraction.hpp:13):
+    the top half of the 32-bit position range through every vectorised / flat
+    query path, both endpoint sorts and the multi-level [32, 512] solve."""
+    torch = pytest.importorskip("torch")
+    from paper_1706_06940_b200 import _lib
+    L = _lib.lib()
+    n = (1 << 31) + 4099
+    A = np.empty(n, np.int32)
+    assert L.brmq_workload_array(1, n, 1706069499, A.ctypes.data, 0) == 0  # ties: values in [0, 16)
+    # a planted unique minimum above 2^31 and one exactly at 2^31
+    A[(1 << 31) + 1000] = -5
+    A[1 << 31] = -3
+    r = np.random.default_rng(2 ** 31)
+    top = 1 << 31
+    qs = [
+        r.integers(0, n, (2000, 2)),                                     # uniform
+        top - 600 + r.integers(0, 1200, (1000, 2)),                      # straddle 2^31
+        n - 1 - r.integers(0, 3000, (1000, 2)),                          # the last blocks
+        np.stack([r.integers(top, n, 1000), r.integers(top, n, 1000)], 1),  # top half only
+    ]
+    sh = r.integers(top, n - 600, 1000)                                  # short, in-block
+    qs.append(np.stack([sh, sh + r.integers(0, 600, 1000)], 1))
+    Q = np.concatenate(qs).astype(np.uint64)
+    Q = np.stack([Q.min(1), Q.max(1)], 1).astype(np.uint64)
+    want = orc.solve_oracle(A, Q)
+    dA = torch.from_numpy(A).cuda()
+    del A
+    dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+    out = torch.empty(Q.shape[0], dtype=torch.int64, device="cuda")
+    for variant in ("bbst", "bbst_ml", "con_bitmap", "con_radix"):
+        out.fill_(-1)
+        _solve_into(engine, variant, dA, dQ, out)
+        got = out.cpu().numpy().view(np.uint64)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (variant, bad[:5], Q[bad[:5]])
+    assert (want[(Q[:, 0] <= top + 1000) & (Q[:, 1] >= top + 1000)] == top + 1000).all()
+    del dA
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------ stage parity
 def test_stage_collect_sort(engine, orc):
     import ctypes as C
