@@ -456,6 +456,104 @@ def run_ours(args) -> dict:
     return rec if rank == 0 else None
 
 
+def run_shard(args) -> dict | None:
+    """--shard: one array split over the ranks.  Rank g holds the
+    contiguous shard g of an array of N x n(config) elements (weak scaling: the
+    shard per GPU is the config's n, the batch is N x q(config) queries over the
+    whole array); every step is one sharded BbST_CON solve per rank
+    (brmq_solve_bbst_con_shard on device buffers) plus ONE NCCL all_reduce(MIN)
+    of the q packed keys (8q bytes), which leaves the answers on every rank."""
+    import torch
+    from paper_1706_06940_b200 import Engine, SortKind, _lib
+    from paper_1706_06940_b200 import shard as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+    name = args.config
+    ak, n0, qk, q0, c, _, desc = CONFIGS[name]
+    if ak not in (0, 1):
+        raise SystemExit(f"--shard: config {name}'s array is not slice-generated")
+    n_total, q = n0 * world, q0 * world
+    off, ns = S.shard_bounds(n_total, world, rank)
+    L = _lib.lib()
+    A = np.empty(ns, np.int32)
+    assert L.brmq_workload_array_range(ak, n_total, SEED0 + c, off, ns, A.ctypes.data, 0) == 0
+    Q = np.empty((q, 2), np.uint64)
+    assert L.brmq_workload_queries(qk, n_total, q, SEED0 + c, Q.ctypes.data, 0) == 0
+    eng = Engine(local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    dA = torch.from_numpy(A).to(dev)
+    dQ = torch.from_numpy(Q.view(np.int64)).to(dev)
+    dK = torch.empty(q, dtype=torch.int64, device=dev)
+    flush = L2Flush(torch, dev)
+
+    def step():
+        return S.solve_sharded(eng, dA, dQ, off, n_total, 512, contraction=True,
+                               sort_kind=SortKind.Bitmap, out=dK)
+
+    want = None
+    if rank == 0 and not args.no_cpu and n_total * 4 <= (4 << 30):
+        import oracle
+        Afull = np.empty(n_total, np.int32)
+        assert L.brmq_workload_array(ak, n_total, SEED0 + c, Afull.ctypes.data, 0) == 0
+        want = oracle.solve_oracle(Afull, Q)
+        del Afull
+    for _ in range(max(args.warmup, 3)):
+        flush()
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = []
+    for _ in range(args.steps):
+        dK.fill_(-1)
+        flush()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record(stream)
+        ans = step()
+        e_.record(stream)
+        e_.synchronize()
+        ms.append(s_.elapsed_time(e_))
+    torch.cuda.synchronize()
+    ok = None
+    if want is not None:
+        ok = bool(np.array_equal(ans.cpu().numpy().view(np.uint64), want))
+        assert ok, "sharded answers differ from the reference oracle"
+    t = max_over_ranks(statistics.mean(ms), dist, dev)
+    dist.barrier()
+    backend = dist.get_backend()
+    eng.close()
+    dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {
+        "metric": metric_name(), "value": q / (t * 1e-3), "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": f"{name} sharded: {desc}; array of N x n elements split in N "
+                               f"contiguous shards, N x q queries over the whole array",
+                   "n_total": n_total, "n_per_gpu": n0, "q": q, "k": 512, "seed": SEED0 + c,
+                   "l2": "flushed before every step, outside the timed window",
+                   "parallelism": f"shard{world} (SURVEY 8e: per-shard BbST_CON + one NCCL "
+                                  "all_reduce(MIN) of packed keys)"},
+        "variant": "con_bitmap_shard",
+        "comm": {"collective": "all_reduce(MIN) int64", "bytes_per_step": 8 * q,
+                 "backend": backend},
+        "bit_exact_vs_reference": ok,
+    }
+
+
 def run_sweep(eng, torch, stream, flush, dA, A, args) -> list:
     """North-star sweep: end-to-end queries/s at n = 1e8 for q = 1e3 .. 1e7, every
     variant (device-resident inputs).  The answer buffer is poisoned before every
@@ -539,6 +637,8 @@ def main() -> None:
     ap.add_argument("--variant", choices=["con_radix", "con_bitmap", "bbst"], default=None)
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / oracle gate")
+    ap.add_argument("--shard", action="store_true",
+                    help="one array split over the ranks + one NCCL min-allreduce per step (SURVEY 8e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
@@ -546,7 +646,7 @@ def main() -> None:
             return
         print(json.dumps(run_reference(args)))
         return
-    rec = run_ours(args)
+    rec = run_shard(args) if args.shard else run_ours(args)
     if rec is not None:
         print(json.dumps(rec))
 

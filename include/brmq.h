@@ -119,7 +119,9 @@ int brmq_solve_bbst_con(brmq_ctx* ctx, const int32_t* A, uint64_t n, const brmq_
  * or UINT64_MAX when the query misses the shard.  The answer of query i over
  * the whole array is (uint32)(min over shards of keys[i]) -- one min-allreduce
  * of q uint64 (NCCL over NVLink) combines the devices exactly.  Query bounds
- * are checked against n_total (BRMQ_ERANGE). */
+ * are checked against n_total (BRMQ_ERANGE).  n_shard may be 0 (a rank left
+ * without elements when the world size does not divide n_total): every key is
+ * then UINT64_MAX, so that rank still joins the collective. */
 int brmq_solve_bbst_shard(brmq_ctx* ctx, const int32_t* A, uint64_t n_shard, uint64_t offset,
                           uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
                           uint64_t* keys, uint32_t flags);

@@ -37,6 +37,10 @@ enum brmq_query_kind {
 
 /* out: n int32 values.  threads = 0 -> all hardware threads. */
 int brmq_workload_array(int kind, uint64_t n, uint64_t seed, int32_t* out, unsigned threads);
+/* out: elements [first, first + count) of the array above (kinds UNIFORM31 and
+ * TIES16 only; a sharded run generates just its own shard). */
+int brmq_workload_array_range(int kind, uint64_t n, uint64_t seed, uint64_t first, uint64_t count,
+                              int32_t* out, unsigned threads);
 /* out: q {left, right} uint64 pairs (== brmq_query). */
 int brmq_workload_queries(int kind, uint64_t n, uint64_t q, uint64_t seed, uint64_t* out,
                           unsigned threads);

@@ -74,6 +74,8 @@ SIGNATURES = {
     "brmq_memcpy": (C.c_int, [vp, vp, vp, C.c_size_t, C.c_int]),
     "brmq_synchronize": (C.c_int, [vp]),
     "brmq_workload_array": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, vp, C.c_uint]),
+    "brmq_workload_array_range": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp,
+                                            C.c_uint]),
     "brmq_workload_queries": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, vp, C.c_uint]),
     "brmq_workload_mix64": (C.c_uint64, [C.c_uint64]),
     # include/brmq_harness.h

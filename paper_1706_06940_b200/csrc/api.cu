@@ -95,6 +95,8 @@ struct brmq_ctx {
     char* st = nullptr;  // grow-only arena that only ever holds epoch-tagged status words
     size_t st_cap = 0;   // (so stale bytes can never alias a live epoch); zeroed on growth
     uint32_t* bitmap = nullptr;  // persistent, kept all-zero by the contraction kernel
+    char* aux = nullptr;  // grow-only buffers of the sharded solves (clipped queries, keys)
+    size_t aux_cap = 0;
     size_t bitmap_words = 0;
     Control* ctl_host = nullptr;  // pinned, device-mapped mirror of the control header
     uint32_t* ctl_host_dev = nullptr;  // its device address (solves publish into it)
@@ -404,6 +406,7 @@ void brmq_ctx_destroy(brmq_ctx* c) {
     if (c->ws) cudaFree(c->ws);
     if (c->st) cudaFree(c->st);
     if (c->bitmap) cudaFree(c->bitmap);
+    if (c->aux) cudaFree(c->aux);
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -517,7 +520,7 @@ template <class Local>
 int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset, uint64_t n_total,
                 const brmq_query* Q, uint64_t q, uint64_t* keys, uint32_t flags, Local local) {
     if (n_total > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
-    if (n_shard == 0 || offset + n_shard > n_total)
+    if (offset + n_shard > n_total)
         return fail(BRMQ_EINVAL, "shard [%llu, %llu) outside the array of %llu",
                     (unsigned long long)offset, (unsigned long long)(offset + n_shard),
                     (unsigned long long)n_total);
@@ -525,12 +528,21 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     CUDA_TRY(cudaSetDevice(c->device));
     const bool dev = is_device(flags);
     cudaStream_t s = c->stream;
-    // the local solve owns the context workspace: the shard's own buffers are
-    // stream-ordered allocations
+    // the local solve owns the context workspace: the shard's own buffers live in
+    // a separate grow-only arena (steady-state calls allocate nothing)
     const size_t a_bytes = (n_shard * 4 + 15) & ~size_t(15);  // keeps the copied queries 16-byte aligned
     const size_t bytes = q * 16 + q * 8 + q * 8 + q + 96 + (dev ? 0 : a_bytes + q * 16);
-    char* buf = nullptr;
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s));
+    if (bytes > c->aux_cap) {
+        drop_graphs(c);  // captured local solves may point into the old arena
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (c->aux) cudaFree(c->aux);
+        c->aux = nullptr;
+        c->aux_cap = 0;
+        const size_t cap = align_up(bytes + bytes / 8, 1 << 21);
+        CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&c->aux), cap));
+        c->aux_cap = cap;
+    }
+    char* buf = c->aux;
     auto* Ql = reinterpret_cast<ulonglong2*>(buf);
     auto* loc = reinterpret_cast<uint64_t*>(buf + q * 16);
     auto* dkeys = reinterpret_cast<uint64_t*>(buf + q * 24);
@@ -549,7 +561,9 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
     const unsigned g = unsigned((q + 255) / 256);
     k_shard_local<<<g, 256, 0, s>>>(dQ, q, offset, n_shard, n_total, Ql, empty, err);
-    int rc = local(dA, reinterpret_cast<const brmq_query*>(Ql), loc);
+    // an empty shard (world does not divide n evenly) answers NO_KEY for every
+    // query: k_shard_local marks them all empty, no local solve runs
+    int rc = n_shard ? local(dA, reinterpret_cast<const brmq_query*>(Ql), loc) : BRMQ_OK;
     if (rc == BRMQ_OK) {
         k_shard_keys<<<g, 256, 0, s>>>(loc, empty, dA, offset, q, dev ? keys : dkeys);
         uint32_t herr = 0;
@@ -559,7 +573,6 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
         herr = *reinterpret_cast<uint32_t*>(c->ctl_host);
         if (herr) rc = fail(BRMQ_ERANGE, "query exceeds array bounds");
     }
-    cudaFreeAsync(buf, s);
     CUDA_TRY(cudaStreamSynchronize(s));
     return rc;
 }

@@ -118,6 +118,30 @@ int brmq_workload_array(int kind, uint64_t n, uint64_t seed, int32_t* out, unsig
     }
 }
 
+int brmq_workload_array_range(int kind, uint64_t n, uint64_t seed, uint64_t first, uint64_t count,
+                              int32_t* out, unsigned threads) {
+    // elements [first, first + count) of brmq_workload_array(kind, n, seed): the
+    // counter-based draws make any slice independent of the rest (a sharded run
+    // generates only its own shard)
+    if (count == 0) return 0;
+    if (!out || first + count > n) return 3;
+    const uint64_t base = stream_base(seed, 0);
+    switch (kind) {
+        case BRMQ_ARRAY_UNIFORM31:
+            par_for(count, threads, [&](uint64_t b, uint64_t e, uint64_t) {
+                for (uint64_t i = b; i < e; ++i) out[i] = int32_t(draw(base, first + i) >> 33);
+            });
+            return 0;
+        case BRMQ_ARRAY_TIES16:
+            par_for(count, threads, [&](uint64_t b, uint64_t e, uint64_t) {
+                for (uint64_t i = b; i < e; ++i) out[i] = int32_t(draw(base, first + i) >> 60);
+            });
+            return 0;
+        default:
+            return 3;  // the walk and the permutation are not slice-local
+    }
+}
+
 int brmq_workload_queries(int kind, uint64_t n, uint64_t q, uint64_t seed, uint64_t* out,
                           unsigned threads) {
     if (q == 0) return 0;

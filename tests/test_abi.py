@@ -131,3 +131,20 @@ def test_workload_threads_deterministic():
     L.brmq_workload_array(2, a1.shape[0], 7, a1.ctypes.data, 1)
     L.brmq_workload_array(2, a2.shape[0], 7, a2.ctypes.data, 8)
     assert np.array_equal(a1, a2)
+
+
+def test_workload_array_range_is_a_slice():
+    """brmq_workload_array_range (sharded runs generate only their shard) equals
+    the same slice of the whole array; kinds without slice locality are refused."""
+    L = _lib.lib()
+    n, seed = 300_001, 1706069402
+    for kind in (0, 1):
+        full = np.empty(n, np.int32)
+        assert L.brmq_workload_array(kind, n, seed, full.ctypes.data, 0) == 0
+        for first, count in ((0, n), (0, 1), (12345, 100_000), (n - 7, 7)):
+            part = np.empty(count, np.int32)
+            assert L.brmq_workload_array_range(kind, n, seed, first, count, part.ctypes.data, 3) == 0
+            assert np.array_equal(part, full[first:first + count])
+    part = np.empty(10, np.int32)
+    assert L.brmq_workload_array_range(2, n, seed, 0, 10, part.ctypes.data, 0) != 0
+    assert L.brmq_workload_array_range(0, n, seed, n - 5, 10, part.ctypes.data, 0) != 0

@@ -73,6 +73,114 @@ def test_sharded_combine_gloo():
     assert res[0] == res[1] == want.tolist()
 
 
+class _StandInEngine:
+    """numpy stand-in for the device shard solves (host-logic tests only): the
+    same call shapes as Engine.solve_batch_bbst[_con]_shard, CPU tensors in and out."""
+
+    def __init__(self, A):
+        self.A = A
+
+    def _keys(self, shard, batch, offset):
+        import torch
+        Q = batch.numpy().view(np.uint64) if isinstance(batch, torch.Tensor) else batch
+        k = shard_keys_reference(self.A, Q, offset, int(shard.shape[0]))
+        return torch.from_numpy(k.view(np.int64)) if isinstance(batch, torch.Tensor) else k
+
+    def solve_batch_bbst_shard(self, shard, batch, offset, n_total, k=512, out=None):
+        return self._keys(shard, batch, offset)
+
+    def solve_batch_bbst_con_shard(self, shard, batch, offset, n_total, k=512, sort_kind=None, out=None):
+        return self._keys(shard, batch, offset)
+
+
+def _worker_tensor(rank, world, port, out):
+    """solve_sharded with tensors (the device path's call sequence, gloo on CPU):
+    world 4 over n = 9 leaves rank 3 with an empty shard, which must still join
+    the collective with all-NO_KEY keys."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    for n in (9, 3001):
+        r = np.random.default_rng(n)
+        A = r.integers(-5, 5, n).astype(np.int32)
+        Q = r.integers(0, n, (300, 2)).astype(np.uint64)
+        off, ns = S.shard_bounds(n, world, rank)
+        eng = _StandInEngine(A)
+        shard = torch.from_numpy(A[off:off + ns].copy())
+        tq = torch.from_numpy(Q.view(np.int64).copy())
+        ans = S.solve_sharded(eng, shard, tq, off, n, contraction=(n == 9))
+        assert isinstance(ans, torch.Tensor) and ans.dtype == torch.int64
+        res[n] = (ns, ans.numpy().astype(np.uint64).tolist())
+    out[rank] = res
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_tensor_path_gloo_empty_shard():
+    world = 4
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_tensor, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert res[3][9][0] == 0  # the empty shard
+    for n in (9, 3001):
+        r = np.random.default_rng(n)
+        A = r.integers(-5, 5, n).astype(np.int32)
+        Q = r.integers(0, n, (300, 2)).astype(np.uint64)
+        want = oracle.naive_numpy(A, Q).tolist()
+        for rank in range(world):
+            assert res[rank][n][1] == want, (n, rank)
+
+
+def _worker_nccl(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    from paper_1706_06940_b200 import Engine
+    r = np.random.default_rng(11)
+    n = 1_000_003
+    A = r.integers(0, 1 << 20, n).astype(np.int32)
+    Q = r.integers(0, n, (50_000, 2)).astype(np.uint64)
+    off, ns = S.shard_bounds(n, world, rank)
+    eng = Engine(rank)
+    dA = torch.from_numpy(A[off:off + ns].copy()).cuda()
+    dQ = torch.from_numpy(Q.view(np.int64).copy()).cuda()
+    for con in (False, True):
+        ans = S.solve_sharded(eng, dA, dQ, off, n, 512, contraction=con)
+        assert ans.is_cuda
+        out[(rank, con)] = ans.cpu().numpy().astype(np.uint64).tolist()
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_two_gpus(orc):
+    """The device combine: keys stay on each GPU, one NCCL all_reduce(MIN)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL min-allreduce across devices)")
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_nccl, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    r = np.random.default_rng(11)
+    n = 1_000_003
+    A = r.integers(0, 1 << 20, n).astype(np.int32)
+    Q = r.integers(0, n, (50_000, 2)).astype(np.uint64)
+    want = orc.solve_oracle(A, Q).tolist()
+    for key, got in res.items():
+        assert got == want, key
+
+
 def test_signed_mapping_preserves_order():
     r = np.random.default_rng(1)
     k = r.integers(0, 2**63, 1000, dtype=np.uint64) * np.uint64(2) + r.integers(0, 2, 1000).astype(np.uint64)
@@ -116,3 +224,36 @@ def test_shard_solve_gpu(engine, orc, variant):
                 assert np.array_equal(kr[:300], shard_keys_reference(A, Q[:300], off, ns))
             keys = np.minimum(keys, kr)
         assert np.array_equal(S.keys_to_answers(keys), want), kind
+        # an empty shard (n_shard = 0) answers NO_KEY for every query
+        empty = (engine.solve_batch_bbst_shard(A[:0], Q, n, n, 512) if variant == "bbst" else
+                 engine.solve_batch_bbst_con_shard(A[:0], Q, n, n, 512,
+                                                   SortKind.Bitmap if variant == "con_bitmap" else SortKind.Radix))
+        assert (empty == S.NO_KEY).all()
+
+
+@pytest.mark.gpu
+def test_shard_solve_device_tensors(engine, orc):
+    """Device-resident shards and keys (the NCCL path's inputs), one process:
+    the combine is done with the same sign-flip the collective uses."""
+    import torch
+    r = np.random.default_rng(9)
+    n = 500_009
+    A = r.integers(0, 100, n).astype(np.int32)
+    Q = r.integers(0, n, (30_000, 2)).astype(np.uint64)
+    want = orc.solve_oracle(A, Q)
+    dQ = torch.from_numpy(Q.view(np.int64).copy()).cuda()
+    world = 4
+    acc = None
+    for rank in range(world):
+        off, ns = S.shard_bounds(n, world, rank)
+        dA = torch.from_numpy(A[off:off + ns].copy()).cuda()
+        for con in (False, True):
+            k = S.local_keys(engine, dA, dQ, off, n, 512, contraction=con)
+            assert k.is_cuda and k.dtype == torch.int64
+            kf = k ^ (-(1 << 63))
+            if con:
+                assert torch.equal(kf, prev)
+            prev = kf
+        acc = kf if acc is None else torch.minimum(acc, kf)
+    got = S.keys_to_answers(acc ^ (-(1 << 63))).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, want)
