@@ -38,7 +38,7 @@ enum brmq_algo {
  * input and their share of 4n bytes in percent.
  *   bbst      : 8 * cells(n, k),  cells(m, k) = ceil(m/k) * (floor_log2(ceil(m/k)) + 1)
  *   bbst-con  : 20 * 2q + 8 * cells(2q, k)   (8 B endpoint pair + 4 B A_Q value + 8 B origin per endpoint)
- *   bbst-ml   : 8 * ceil(n / k_1) (level-1 keys, h = 2) + 8 * cells(n, k_h)
+ *   bbst-ml   : 8 * sum_{j < h-1} ceil(n / k_j) (the keys of every lower level) + 8 * cells(n, k_h)
  *   sparse    : 4 * sum_e (n - 2^e + 1)      (element_sparse_table.cpp:16-31 jagged uint32 rows)
  *   st-rmq-con: n/8 (mark bits) + 12 * M + 4 * sum_e (M - 2^e + 1), M = 4q + 1
  *   naive     : 0
@@ -51,6 +51,14 @@ int brmq_account_memory(int algo, uint64_t n, uint64_t q, const uint32_t* ks, ui
  * on the checksum even where tie positions could differ. */
 int brmq_answers_checksum(const int32_t* A, uint64_t n, const uint64_t* answers, uint64_t q,
                           uint64_t* out);
+
+/* emit_plot: reads the records of a harness CSV (the emit_csv
+ * columns) and writes a self-contained SVG with one time-vs-q line per
+ * algorithm series (algo + k_chain), q on a log scale, t_total_ns on a log
+ * scale.  Deterministic for fixed records.  Records must share n (BRMQ_EINVAL
+ * otherwise); an empty record set writes nothing and returns BRMQ_OK with a
+ * warning on stderr.  BRMQ_EIO when a file cannot be read or written. */
+int brmq_emit_plot(const char* csv_path, const char* svg_path);
 
 /* File I/O.  Readers with a NULL buffer only report the count. BRMQ_EIO on I/O
  * failure, BRMQ_EINVAL on a bad magic / version / truncated body or when the

@@ -88,6 +88,7 @@ SIGNATURES = {
     "brmq_read_query_file": (C.c_int, [C.c_char_p, vp, C.c_uint64, u64p]),
     "brmq_write_answer_file": (C.c_int, [C.c_char_p, vp, C.c_uint64]),
     "brmq_read_answer_file": (C.c_int, [C.c_char_p, vp, C.c_uint64, u64p]),
+    "brmq_emit_plot": (C.c_int, [C.c_char_p, C.c_char_p]),
     "brmq_verify_answers": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, vp, C.c_uint, u64p, u64p]),
 }
 

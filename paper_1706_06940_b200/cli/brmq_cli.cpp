@@ -80,7 +80,7 @@ int usage() {
             "usage: brmq gen-array --n N --seed S --out F [--kind permutation|uniform|ties16|walk]\n"
             "       brmq gen-queries --n N --q Q --seed S --out F [--kind uniform|loguniform|mixed]\n"
             "       brmq run --algo {naive|sparse|st-rmq-con|bbst-con|bbst|bbst-ml} --array F\n"
-            "                --queries F [--k K | --chain K1,K2,...] [--runs R] [--threads T]\n"
+            "                --queries F [--k K | --chain K1,K2,...] [--runs R (odd)] [--threads T]\n"
             "                [--sort radix|comparison|bitmap] --csv F [--plot F] [--answers F]\n"
             "       brmq verify --array F --queries F --answers F [--threads T]\n");
     return 1;
@@ -171,7 +171,7 @@ int cmd_run(const Args& a) {
     const int sort_kind = sort == "radix" ? BRMQ_SORT_RADIX
                         : sort == "comparison" ? BRMQ_SORT_COMPARISON
                         : sort == "bitmap" ? BRMQ_SORT_BITMAP : -1;
-    if (sort_kind < 0 || runs == 0) return usage();
+    if (sort_kind < 0 || runs == 0 || runs % 2 == 0) return usage();  // odd: the median is one run
     const std::vector<int32_t> A = load_array(a.get("array"));
     const std::vector<brmq_query> Q = load_queries(a.get("queries"));
     const uint64_t n = A.size(), q = Q.size();
@@ -263,7 +263,7 @@ int cmd_run(const Args& a) {
             (unsigned long long)runs, median(t_sort), median(t_con), median(t_build), median(t_ans),
             median(t_tot), (unsigned long long)extra, pct, (unsigned long long)checksum);
     fclose(f);
-    if (a.has("plot")) fprintf(stderr, "brmq: --plot is not supported by this build (CSV written)\n");
+    if (a.has("plot")) check(brmq_emit_plot(csv.c_str(), a.get("plot").c_str()), "plot");
     return 0;
 }
 

@@ -56,7 +56,7 @@ inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a
 struct Control {
     uint32_t err;       // 1 query out of range (direct), 2 range (collect/unique), 4 unsorted, 8 logic
     uint32_t span[2];   // [~min endpoint, max endpoint]
-    uint32_t tickets[5];  // last-CTA tickets: [0] k_unique, [4] publish
+    uint32_t tickets[5];  // last-CTA tickets: [0] k_unique
     uint64_t nb;        // |boundary|
     uint64_t aq_len;    // |A_Q|
     uint64_t b_dev;     // blocks over A_Q
@@ -104,6 +104,8 @@ struct brmq_ctx {
     uint32_t* epoch_dev = nullptr;  // device epoch counter, bumped by every solve (graph-safe)
     uint32_t epoch_host = 1;        // host mirror of *epoch_dev
     bool use_graphs = true;
+    bool use_pdl = false;  // programmatic dependent launches inside a solve (BRMQ_PDL=1: on; DESIGN 3.5)
+    bool use_fuse = true;  // small A_Q: block minima + table inside the contraction (BRMQ_FUSE=0: off)
     struct GraphEntry;
     std::vector<GraphEntry*> graphs;
     // timing: 0 off, 1 every stage, 2 only the roofline kernel (contract / block_argmin)
@@ -191,7 +193,10 @@ int ensure_bitmap(brmq_ctx* c, uint64_t n) {
     return BRMQ_OK;
 }
 
-__global__ void k_bump_epoch(uint32_t* epoch, uint32_t by) { *epoch += by; }
+__global__ void k_bump_epoch(uint32_t* epoch, uint32_t by) {
+    brmq::pdl_wait();
+    *epoch += by;
+}
 
 // Every solve reserves `count` consecutive 24-bit epochs for its single-pass
 // scans: one tiny kernel bumps the device counter first, and each look-back
@@ -392,6 +397,8 @@ int brmq_ctx_create(brmq_ctx** out, int device) {
         return fail(BRMQ_ECUDA, "epoch counter allocation failed");
     }
     if (const char* g = getenv("BRMQ_GRAPHS")) c->use_graphs = atoi(g) != 0;
+    if (const char* g = getenv("BRMQ_PDL")) c->use_pdl = atoi(g) != 0;
+    if (const char* g = getenv("BRMQ_FUSE")) c->use_fuse = atoi(g) != 0;
     *out = c;
     return BRMQ_OK;
 }
@@ -471,10 +478,22 @@ int brmq_synchronize(brmq_ctx* c) {
 // The final kernel also re-zeroes the accumulating fields (err, span, tickets) for
 // the next solve, so a solve's graph needs no memset node; prepare_ctl zeroes the
 // header explicitly (outside any graph) only when something else left it dirty.
-brmq::CtlPublish publish(brmq_ctx* c, Control* ctl) {
-    return brmq::CtlPublish{reinterpret_cast<const uint32_t*>(ctl), c->ctl_host_dev,
-                            &ctl->tickets[4], uint32_t(kCtlHeader / 4),
-                            uint32_t(offsetof(Control, nb) / 4)};
+// One warp, launched after the final kernel (stream order: every CTA of it has
+// finished): the query kernels carry no end-of-kernel barrier + ticket for this
+// (measured: ~1 us more lifetime per CTA, 78K CTAs at c3).
+__global__ void k_publish(const uint32_t* __restrict__ ctl, uint32_t* __restrict__ host, uint32_t words,
+                          uint32_t reset_words) {
+    brmq::pdl_wait();
+    for (uint32_t i = threadIdx.x; i < words; i += 32) host[i] = __ldcg(ctl + i);
+    __syncwarp();
+    for (uint32_t i = threadIdx.x; i < reset_words; i += 32) const_cast<uint32_t*>(ctl)[i] = 0u;
+    __threadfence_system();
+}
+
+int publish(brmq_ctx* c, Control* ctl, cudaStream_t s) {
+    brmq::launch_k(k_publish, dim3(1), dim3(32), 0, s, reinterpret_cast<const uint32_t*>(ctl),
+                   c->ctl_host_dev, uint32_t(kCtlHeader / 4), uint32_t(offsetof(Control, nb) / 4));
+    return 1;
 }
 
 int prepare_ctl(brmq_ctx* c, Control* ctl) {
@@ -490,6 +509,7 @@ int prepare_ctl(brmq_ctx* c, Control* ctl) {
 __global__ void k_shard_local(const ulonglong2* __restrict__ Q, uint64_t q, uint64_t off,
                               uint64_t ns, uint64_t n_total, ulonglong2* __restrict__ Ql,
                               uint8_t* __restrict__ empty, uint32_t* __restrict__ err) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= q) return;
     const ulonglong2 x = __ldg(Q + i);
@@ -505,6 +525,7 @@ __global__ void k_shard_local(const ulonglong2* __restrict__ Q, uint64_t q, uint
 __global__ void k_shard_keys(const uint64_t* __restrict__ loc, const uint8_t* __restrict__ empty,
                              const int32_t* __restrict__ A, uint64_t off, uint64_t q,
                              uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= q) return;
     const uint64_t p = loc[i];
@@ -560,12 +581,12 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     }
     CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
     const unsigned g = unsigned((q + 255) / 256);
-    k_shard_local<<<g, 256, 0, s>>>(dQ, q, offset, n_shard, n_total, Ql, empty, err);
+    brmq::launch_k(k_shard_local, dim3(g), dim3(256), 0, s, dQ, q, offset, n_shard, n_total, Ql, empty, err);
     // an empty shard (world does not divide n evenly) answers NO_KEY for every
     // query: k_shard_local marks them all empty, no local solve runs
     int rc = n_shard ? local(dA, reinterpret_cast<const brmq_query*>(Ql), loc) : BRMQ_OK;
     if (rc == BRMQ_OK) {
-        k_shard_keys<<<g, 256, 0, s>>>(loc, empty, dA, offset, q, dev ? keys : dkeys);
+        brmq::launch_k(k_shard_keys, dim3(g), dim3(256), 0, s, loc, empty, dA, offset, q, dev ? keys : dkeys);
         uint32_t herr = 0;
         if (!dev) CUDA_TRY(cudaMemcpyAsync(keys, dkeys, q * 8, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaMemcpyAsync(c->ctl_host, err, 4, cudaMemcpyDeviceToHost, s));
@@ -635,6 +656,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
@@ -643,9 +665,10 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
             tm.end(0);
         }
         tm.stage("query", launches);
-        const int l = brmq::launch_naive(dA, n, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
+        const int l = brmq::launch_naive(dA, n, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -702,6 +725,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         int l = 0;
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
@@ -719,9 +743,10 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
+        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -789,6 +814,7 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         int l = 0;
         if (!dev) {
             tm.stage("h2d", launches);
@@ -809,9 +835,10 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_chain(dA, n, ks, h, M, ST, b, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
+        l = brmq::launch_query_chain(dA, n, ks, h, M, ST, b, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -878,6 +905,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     cudaStream_t s = c->stream;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         int l = 0;
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
@@ -895,9 +923,10 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_ml(dA, n, k, ST, b, SUB, dQ, q, dAns, &ctl->err, s, publish(c, ctl));
+        l = brmq::launch_query_ml(dA, n, k, ST, b, SUB, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -953,28 +982,33 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
 
     Carve cv;
     const size_t i_ctl = cv.add(sizeof(Control));
-    const size_t i_cl = cv.add(q * 4);
-    const size_t i_cr = cv.add(q * 4);
     const size_t i_aq = cv.add((aq_max + 2) * 8);
     const size_t i_st = cv.add(size_t(L) * b_max * 8);
     // power-of-two k in [64, 512]: 32-key sub-block minima over A_Q as a second level
     // (answers identical; partial blocks are resolved through them, DESIGN 3.2)
     const bool sub_level = k >= 64 && k <= 512 && (k & (k - 1)) == 0;
-    const size_t i_sub = cv.add(sub_level ? ((aq_max + 31) / 32 + 2) * 8 : 0);
+    const size_t sub_words = (aq_max + 31) / 32 + 2;
+    const size_t i_sub = cv.add(sub_level ? sub_words * 8 : 0);
+    // small A_Q: the contraction itself yields the block / sub-block minima
+    // (brmq::ContractFuse); no block-argmin pass over A_Q follows.  Large A_Q (dense
+    // areas: many reductions on each block key) keeps the separate pass.
+    const bool fuse = sub_level && b_max <= 1024 && c->use_fuse;  // (c4-con, 3906 blocks: +25 us of reductions for -12 us)
     Carve sv;  // status arena
     const size_t i_cst = sv.add(brmq::contract_status_words() * 8);
     const size_t i_pc = cv.add(size_t(brmq::kMaxContractRanges) * brmq::kContractWarps * 4);
-    size_t i_k0 = 0, i_v0 = 0, i_k1 = 0, i_v1 = 0, i_rs = 0, i_rst = 0, i_ust = 0, i_wi = 0;
-    if (use_bitmap) {
-        i_wi = cv.add((n / 32 + 2) * 8);
-    } else {
+    // both pipelines: the contraction emits (rank prefix, bits) per non-empty bitmap
+    // word and the query kernel computes each query's contracted coordinates from
+    // them (remap_queries_from_sorted, contraction.cpp:174-199, folded into
+    // answering: no random scatter of ranks into per-query arrays)
+    size_t i_k0 = 0, i_k1 = 0, i_rs = 0, i_rst = 0;
+    const size_t i_wi = cv.add((n / 32 + 2) * 8);
+    if (!use_bitmap) {
+        // the radix pipeline sorts the endpoint POSITIONS (keys only): their origins
+        // served only the rank scatter above
         i_k0 = cv.add(m * 4);
-        i_v0 = cv.add(m * 4);
         i_k1 = cv.add(m * 4);
-        i_v1 = cv.add(m * 4);
         i_rs = cv.add(brmq::radix_sort_temp_bytes(m, bits));
         i_rst = sv.add(brmq::radix_sort_status_words(m, bits) * 8);
-        i_ust = sv.add(brmq::unique_status_words(m) * 8);
     }
     const size_t i_a = dev ? 0 : cv.add(n * 4);
     const size_t i_q = dev ? 0 : cv.add(q * 16);
@@ -984,8 +1018,6 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     auto P = [&](size_t i) { return c->ws + cv.off[i]; };
     auto S = [&](size_t i) { return reinterpret_cast<uint64_t*>(c->st + sv.off[i]); };
     auto* ctl = reinterpret_cast<Control*>(P(i_ctl));
-    auto* cl = reinterpret_cast<uint32_t*>(P(i_cl));
-    auto* cr = reinterpret_cast<uint32_t*>(P(i_cr));
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     auto* ST = reinterpret_cast<uint64_t*>(P(i_st));
     auto* cst = S(i_cst);
@@ -994,10 +1026,11 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     const uint64_t* dQ = dev ? reinterpret_cast<const uint64_t*>(Q) : reinterpret_cast<uint64_t*>(P(i_q));
     uint64_t* dAns = dev ? answers : reinterpret_cast<uint64_t*>(P(i_ans));
     cudaStream_t s = c->stream;
-    const uint32_t n_epochs = use_bitmap ? 1u : 2u + uint32_t(brmq::radix_sort_passes(bits));
+    const uint32_t n_epochs = 1u;  // the contraction's look-back (the sort's descriptors are zeroed)
     if (int rc = begin_epochs(c, n_epochs)) return rc;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         int l = 0;
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
@@ -1007,68 +1040,74 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
             tm.end(0);
         }
         // the epochs of this solve are reserved by the first kernel (k_collect)
-        // epoch offsets: 0 contraction, 1 unique, 2.. radix passes
+        // epoch offset 0: the contraction's look-back
+        auto* SUB = reinterpret_cast<uint64_t*>(P(i_sub));
+        uint64_t* fill0 = fuse ? SUB : nullptr;
+        uint64_t* fill1 = fuse ? ST : nullptr;
+        const uint64_t fill0_n = fuse ? sub_words : 0, fill1_n = fuse ? b_max : 0;
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
             l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap,
-                                     ctl->span, &ctl->err, s, c->epoch_dev, n_epochs);
+                                     ctl->span, &ctl->err, s, c->epoch_dev, n_epochs, fill0, fill0_n,
+                                     fill1, fill1_n);
             l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
             launches += l;
             tm.end(l);
         } else {
             auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
-            auto* v0 = reinterpret_cast<uint32_t*>(P(i_v0));
             auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
-            auto* v1 = reinterpret_cast<uint32_t*>(P(i_v1));
             tm.stage("collect", launches);
-            l = brmq::launch_collect(dQ, q, n, k0, v0, nullptr, nullptr, &ctl->err, s,
-                                     c->epoch_dev, n_epochs);
+            l = brmq::launch_collect(dQ, q, n, k0, nullptr, nullptr, nullptr, &ctl->err, s,
+                                     c->epoch_dev, n_epochs, fill0, fill0_n, fill1, fill1_n);
             launches += l;
             tm.end(l);
             tm.stage("radix_sort", launches);
             bool in_alt = false;
-            l = brmq::launch_radix_sort(k0, v0, k1, v1, m, bits, P(i_rs), S(i_rst), s, &in_alt,
+            l = brmq::launch_radix_sort(k0, nullptr, k1, nullptr, m, bits, P(i_rs), S(i_rst), s, &in_alt,
                                         c->epoch_dev, 2);
             launches += l;
             tm.end(l);
+            // dedup: the sorted positions mark the bitmap (coalesced, no look-back);
+            // ranks per contraction piece from the bitmap as in the bitmap pipeline
             tm.stage("unique_rank", launches);
-            l = brmq::launch_unique(in_alt ? k1 : k0, in_alt ? v1 : v0, m, n, nullptr, cl, cr,
-                                    c->bitmap, ctl->rcnt, R, ctl->span, &ctl->nb, &ctl->err, S(i_ust),
-                                    &ctl->tickets[0], c->epoch_dev, 1, s);
+            l = brmq::launch_mark_sorted(in_alt ? k1 : k0, m, n, c->bitmap, ctl->span, &ctl->err, s);
+            l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
             launches += l;
             tm.end(l);
         }
         tm.stage("contract", launches);
-        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, !use_bitmap, AQ,
-                                  &ctl->nb, &ctl->aq_len,
-                                  use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr, cst,
-                                  c->epoch_dev, 0, s, false, use_bitmap ? pcnt : nullptr, 2 * q);
+        const brmq::ContractFuse fz{SUB, ST, b_max, brmq::floor_log2_u64(k), &ctl->b_dev};
+        bool fused = false;
+        l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, false, AQ,
+                                  &ctl->nb, &ctl->aq_len, reinterpret_cast<uint2*>(P(i_wi)), cst,
+                                  c->epoch_dev, 0, s, false, pcnt, 2 * q,
+                                  fuse ? &fz : nullptr, &fused);
         launches += l;
         tm.end(l);
         // (bitmap pipeline: the query remap is folded into the query kernel)
-        auto* SUB = reinterpret_cast<uint64_t*>(P(i_sub));
-        tm.stage("block_argmin", launches);
-        l = sub_level ? brmq::launch_block_argmin_keys_ml(AQ, aq_max, &ctl->aq_len, k, ST, SUB,
-                                                          &ctl->b_dev, s)
-                      : brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
-        launches += l;
-        tm.end(l);
+        if (!fused) {  // (e.g. unaligned A: the filled sub / row 0 are overwritten here)
+            tm.stage("block_argmin", launches);
+            l = sub_level ? brmq::launch_block_argmin_keys_ml(AQ, aq_max, &ctl->aq_len, k, ST, SUB,
+                                                              &ctl->b_dev, s)
+                          : brmq::launch_block_argmin_keys(AQ, aq_max, &ctl->aq_len, k, ST, &ctl->b_dev, s);
+            launches += l;
+            tm.end(l);
+        }
         tm.stage("sparse_table", launches);
         l = brmq::launch_sparse_table(ST, b_max, &ctl->b_dev, s);
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        const uint2* wi = use_bitmap ? reinterpret_cast<uint2*>(P(i_wi)) : nullptr;
+        const uint2* wi = reinterpret_cast<uint2*>(P(i_wi));
         if (sub_level)
-            l = brmq::launch_query_con_flat(AQ, k, ST, b_max, SUB, dQ, wi, cl, cr, n, q, dAns, s,
-                                            publish(c, ctl));
+            l = brmq::launch_query_con_flat(AQ, k, ST, b_max, SUB, dQ, wi, nullptr, nullptr, n, q, dAns, s,
+                                            brmq::CtlPublish{});
         else
-            l = use_bitmap ? brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ, wi, n, q, dAns, s,
-                                                              publish(c, ctl))
-                           : brmq::launch_query_contracted(AQ, &ctl->aq_len, k, ST, b_max, dQ, cl,
-                                                           cr, q, dAns, s, publish(c, ctl));
+            l = brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ, wi, n, q, dAns, s,
+                                                 brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -1158,6 +1197,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     if (int rc = begin_epochs(c, n_epochs)) return rc;
     int launches = 0;
     auto enqueue = [&]() -> int {
+        brmq::PdlScope pdl(c->timing == 0 && c->use_pdl);  // kernels after the first: PDL secondaries
         int l = 0;
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
@@ -1201,9 +1241,10 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_st(dQ, cl, cr, q, ST, e_max, dAns, s, publish(c, ctl));
+        l = brmq::launch_query_st(dQ, cl, cr, q, ST, e_max, dAns, s, brmq::CtlPublish{});
         launches += l;
         tm.end(l);
+        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
@@ -1287,7 +1328,7 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
     brmq::launch_split_eps(dE, m, k0, v0, s);
     bool in_alt = false;
     if (int rc = begin_epochs(c, 4)) return rc;
-    k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, 4);
+    brmq::launch_k(k_bump_epoch, dim3(1), dim3(1), 0, s, c->epoch_dev, 4);
     c->epoch_host += 4;
     brmq::launch_radix_sort(k0, v0, k1, v1, m, 32, P(i_rs), reinterpret_cast<uint64_t*>(c->st), s,
                             &in_alt, c->epoch_dev, 0);
@@ -1345,7 +1386,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     auto* AQ = reinterpret_cast<uint64_t*>(P(i_aq));
     brmq::launch_split_eps(dE, m, k, v, s);
     if (int rc = begin_epochs(c, 2)) return rc;
-    k_bump_epoch<<<1, 1, 0, s>>>(c->epoch_dev, 2);
+    brmq::launch_k(k_bump_epoch, dim3(1), dim3(1), 0, s, c->epoch_dev, 2);
     c->epoch_host += 2;
     uint32_t G = 0, R = 0;
     brmq::contract_partition(n, &G, &R);

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_i32_vec(const int32_t
                                                                    uint64_t n, uint64_t nfull,
                                                                    uint64_t nblk, uint32_t k,
                                                                    uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     if (blk >= nblk) return;
     const unsigned lane = lane_id();
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_i32_gen(const int32_t
                                                                    uint64_t n, uint32_t k,
                                                                    uint64_t first, uint64_t nblk,
                                                                    uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t blk = first + ((uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5);
     if (blk >= nblk) return;
     const unsigned lane = lane_id();
@@ -86,6 +88,8 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys(const uint64_t* 
                                                                 uint32_t k,
                                                                 uint64_t* __restrict__ keys,
                                                                 uint64_t* __restrict__ b_dev) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     const uint64_t len = len_dev ? *len_dev : len_max;
     const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_i32_small(const int32
                                                                      uint64_t n, uint32_t k,
                                                                      uint64_t nblk,
                                                                      uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t blk = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (blk >= nblk) return;
     const uint64_t lo = blk * k, hi = lo + k < n ? lo + k : n;
@@ -139,6 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys_small(const uint
                                                                       uint64_t len, uint32_t k,
                                                                       uint64_t nblk,
                                                                       uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t blk = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (blk >= nblk) return;
     const uint64_t lo = blk * k, hi = lo + k < len ? lo + k : len;
@@ -155,6 +161,7 @@ template <int V>
 __global__ void __launch_bounds__(kThreads) k_block_argmin_i32_grp(const int32_t* __restrict__ A,
                                                                    uint64_t nfull,
                                                                    uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     constexpr int kR = 4;
     const uint64_t warp = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     const unsigned lane = lane_id();
@@ -193,6 +200,7 @@ inline unsigned grid_for_warps(uint64_t warps) {
 
 // k = 1 (the element Sparse Table of the harness's "sparse" algorithm): keys only
 __global__ void k_pack_keys(const int32_t* __restrict__ A, uint64_t n, uint64_t* __restrict__ keys) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) keys[i] = pack_key(__ldg(A + i), uint32_t(i));
 }
@@ -202,7 +210,7 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
     const uint64_t nblk = (n + k - 1) / k;
     if (nblk == 0) return 0;
     if (k == 1) {
-        k_pack_keys<<<unsigned((n + 255) / 256), 256, 0, stream>>>(A, n, keys);
+        brmq::launch_k(k_pack_keys, dim3(unsigned((n + 255) / 256)), dim3(256), 0, stream, A, n, keys);
         return 1;
     }
     const bool al = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
@@ -210,24 +218,24 @@ int launch_block_argmin_i32(const int32_t* A, uint64_t n, uint32_t k, uint64_t* 
         const uint64_t nfull = n / k;
         const unsigned grid = unsigned((nfull * (k / 4) + 32 * 4 * kWarps - 1) / (32 * 4 * kWarps));
         switch (k) {
-            case 4: k_block_argmin_i32_grp<1><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
-            case 8: k_block_argmin_i32_grp<2><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
-            case 16: k_block_argmin_i32_grp<4><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
-            case 32: k_block_argmin_i32_grp<8><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
-            case 64: k_block_argmin_i32_grp<16><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
-            default: k_block_argmin_i32_grp<32><<<grid, kThreads, 0, stream>>>(A, nfull, keys); break;
+            case 4: brmq::launch_k(k_block_argmin_i32_grp<1>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
+            case 8: brmq::launch_k(k_block_argmin_i32_grp<2>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
+            case 16: brmq::launch_k(k_block_argmin_i32_grp<4>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
+            case 32: brmq::launch_k(k_block_argmin_i32_grp<8>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
+            case 64: brmq::launch_k(k_block_argmin_i32_grp<16>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
+            default: brmq::launch_k(k_block_argmin_i32_grp<32>, dim3(grid), dim3(kThreads), 0, stream, A, nfull, keys); break;
         }
         if (nblk > nfull)  // the clipped trailing block
-            k_block_argmin_i32_gen<<<1, kThreads, 0, stream>>>(A, n, k, nfull, nblk, keys);
+            brmq::launch_k(k_block_argmin_i32_gen, dim3(1), dim3(kThreads), 0, stream, A, n, k, nfull, nblk, keys);
         return nblk > nfull ? 2 : 1;
     }
     if (k < 32) {
-        k_block_argmin_i32_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(A, n, k, nblk,
+        brmq::launch_k(k_block_argmin_i32_small, dim3(unsigned((nblk + kThreads - 1) / kThreads)), dim3(kThreads), 0, stream, A, n, k, nblk,
                                                                                                   keys);
     } else if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0) {
-        k_block_argmin_i32_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys);
+        brmq::launch_k(k_block_argmin_i32_vec, dim3(grid_for_warps(nblk)), dim3(kThreads), 0, stream, A, n, n / k, nblk, k, keys);
     } else {
-        k_block_argmin_i32_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, k, 0, nblk, keys);
+        brmq::launch_k(k_block_argmin_i32_gen, dim3(grid_for_warps(nblk)), dim3(kThreads), 0, stream, A, n, k, 0, nblk, keys);
     }
     return 1;
 }
@@ -237,12 +245,12 @@ int launch_block_argmin_keys(const uint64_t* K, uint64_t len_max, const uint64_t
     uint64_t nblk = (len_max + k - 1) / k;
     if (k < 32 && !len_dev && !b_dev) {  // host-known length (multi-level chains)
         if (nblk == 0) return 0;
-        k_block_argmin_keys_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+        brmq::launch_k(k_block_argmin_keys_small, dim3(unsigned((nblk + kThreads - 1) / kThreads)), dim3(kThreads), 0, stream, 
             K, len_max, k, nblk, keys);
         return 1;
     }
     if (nblk == 0) nblk = 1;  // still publish *b_dev
-    k_block_argmin_keys<<<grid_for_warps(nblk), kThreads, 0, stream>>>(K, len_max, len_dev, k, keys,
+    brmq::launch_k(k_block_argmin_keys, dim3(grid_for_warps(nblk)), dim3(kThreads), 0, stream, K, len_max, len_dev, k, keys,
                                                                        b_dev);
     return 1;
 }
@@ -264,6 +272,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_ml_vec(const int32_t*
                                                                   uint64_t nblk, uint32_t k,
                                                                   uint64_t* __restrict__ keys,
                                                                   uint64_t* __restrict__ sub) {
+    brmq::pdl_wait();
     const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     if (blk >= nblk) return;
     const unsigned lane = lane_id();
@@ -312,6 +321,7 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_ml_gen(const int32_t*
                                                                   uint32_t k,
                                                                   uint64_t* __restrict__ keys,
                                                                   uint64_t* __restrict__ sub) {
+    brmq::pdl_wait();
     const uint64_t blk = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     if (blk >= nblk) return;
     const unsigned lane = lane_id();
@@ -336,6 +346,8 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys_ml(
     const uint64_t* __restrict__ K, const uint64_t* __restrict__ len_dev, uint64_t len_max,
     uint32_t k, uint64_t* __restrict__ keys, uint64_t* __restrict__ sub,
     uint64_t* __restrict__ b_dev) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     const uint64_t len = len_dev ? *len_dev : len_max;
     const uint64_t blk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
@@ -375,10 +387,10 @@ int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* k
     const uint64_t nblk = (n + k - 1) / k;
     if (nblk == 0) return 0;
     if ((k & 127u) == 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0)
-        k_block_argmin_ml_vec<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, n / k, nblk, k, keys,
+        brmq::launch_k(k_block_argmin_ml_vec, dim3(grid_for_warps(nblk)), dim3(kThreads), 0, stream, A, n, n / k, nblk, k, keys,
                                                                             sub);
     else
-        k_block_argmin_ml_gen<<<grid_for_warps(nblk), kThreads, 0, stream>>>(A, n, nblk, k, keys, sub);
+        brmq::launch_k(k_block_argmin_ml_gen, dim3(grid_for_warps(nblk)), dim3(kThreads), 0, stream, A, n, nblk, k, keys, sub);
     return 1;
 }
 
@@ -388,14 +400,14 @@ int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint6
     uint64_t nblk = (len_max + k - 1) / k;
     if (k < 32 && !len_dev && !b_dev) {  // host-known length (multi-level chains)
         if (nblk == 0) return 0;
-        k_block_argmin_keys_small<<<unsigned((nblk + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+        brmq::launch_k(k_block_argmin_keys_small, dim3(unsigned((nblk + kThreads - 1) / kThreads)), dim3(kThreads), 0, stream, 
             K, len_max, k, nblk, keys);
         return 1;
     }
     if (nblk == 0) nblk = 1;  // still publish *b_dev
     // few blocks (A_Q of a small batch): one warp per CTA spreads them over all SMs
     const unsigned nt = nblk <= uint64_t(148) * 32 ? 32u : unsigned(kThreads);
-    k_block_argmin_keys_ml<<<unsigned((nblk * 32 + nt - 1) / nt), nt, 0, stream>>>(K, len_dev, len_max,
+    brmq::launch_k(k_block_argmin_keys_ml, dim3(unsigned((nblk * 32 + nt - 1) / nt)), dim3(nt), 0, stream, K, len_dev, len_max,
                                                                                  k, keys, sub, b_dev);
     return 1;
 }

@@ -31,6 +31,14 @@ __host__ __device__ __forceinline__ uint64_t kmin(uint64_t a, uint64_t b) { retu
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// PDL (kernels.h launch_k): the first statement of every kernel.  Waits until
+// the predecessor grid has completed and flushed (a no-op for a plain launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Lets this grid's dependents be scheduled before it exits.  Only in kernels
+// with small grids: every CTA of a large grid paying it cost ~1-2 ns per CTA of
+// serialised front-end work (measured: c5 BbST block argmin, 262K CTAs, +0.55 ms).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Warp-wide min of packed keys with two redux.sync (no 64-bit shuffles):
 // min of the high words, then min of the low words among lanes holding it.
 __device__ __forceinline__ uint64_t warp_min_key(uint64_t k) {
@@ -183,27 +191,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait_sleep(bar, parity)) {
     }
 }
-// The end of a solve: the last CTA of its final kernel copies the control header
-// (errors, sizes) into host-mapped pinned memory, so no device-to-host copy node
-// follows the kernels (a copy node cost ~7 us per solve on this part).
-__device__ __forceinline__ void publish_control(const CtlPublish& p) {
-    if (!p.host) return;
-    __shared__ bool s_last_cta;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();  // this CTA's writes (err bits) before its ticket
-        s_last_cta = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last_cta) return;
-    __threadfence();
-    for (uint32_t i = threadIdx.x; i < p.words; i += blockDim.x) p.host[i] = __ldcg(p.ctl + i);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < p.reset_words; i += blockDim.x)
-        const_cast<uint32_t*>(p.ctl)[i] = 0u;
-    __threadfence_system();
-}
-
 __device__ __forceinline__ uint32_t ld_volatile_shared_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");

@@ -29,6 +29,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kItems = 8;   // 2048-endpoint dedup tiles (measured vs 1024 and 4096)
 constexpr int kTile = kThreads * kItems;
+constexpr int kCollectU = 4;  // queries per thread in flight in k_collect
 
 // ------------------------------------------------------------------ collect
 // span[0] = max(~pos) (= ~min pos), span[1] = max(pos); control block starts zeroed.
@@ -43,7 +44,16 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                                                       uint32_t* __restrict__ err,
                                                       uint32_t* __restrict__ epoch_bump,
                                                       uint32_t epoch_by, uint32_t mark_lo,
-                                                      uint32_t mark_hi) {
+                                                      uint32_t mark_hi, uint64_t* __restrict__ fill0,
+                                                      uint64_t fill0_n, uint64_t* __restrict__ fill1,
+                                                      uint64_t fill1_n) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
+    {
+        const uint64_t t = uint64_t(blockIdx.x) * kThreads + threadIdx.x, nt = uint64_t(gridDim.x) * kThreads;
+        for (uint64_t i = t; i < fill0_n; i += nt) fill0[i] = kNoKey;
+        for (uint64_t i = t; i < fill1_n; i += nt) fill1[i] = kNoKey;
+    }
     // the solve's epoch reservation rides on this first kernel (no extra launch)
     if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) *epoch_bump += epoch_by;
     __shared__ uint32_t s_lo, s_hi;
@@ -51,8 +61,19 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
     __syncthreads();
     uint32_t lo_acc = 0xFFFFFFFFu, hi_acc = 0;
     const uint64_t stride = uint64_t(gridDim.x) * kThreads;
-    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < q; i += stride) {
-        const ulonglong2 x = __ldg(Q + i);
+    // kCollectU queries per thread in flight (ncu, c5-con: 75% of the stall
+    // samples waited on the single streamed query load of the plain loop)
+    constexpr int U = kCollectU;
+    for (uint64_t i0 = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i0 < q; i0 += U * stride) {
+      ulonglong2 xs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+          xs[u] = i0 + u * stride < q ? __ldcs(Q + i0 + u * stride) : make_ulonglong2(0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * stride;
+        if (i >= q) break;
+        const ulonglong2 x = xs[u];
         uint64_t l = x.x, r = x.y;
         if (l > r) { const uint64_t t = l; l = r; r = t; }  // types.hpp:18-20
         if (r >= n) {                                        // naive.hpp:14-15 (range)
@@ -61,17 +82,17 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
             if (l > r) l = r;
         }
         const uint32_t lo = uint32_t(l), hi = uint32_t(r);
-        if (keys) {
-            reinterpret_cast<uint2*>(keys)[i] = make_uint2(lo, hi);
+        if (keys) reinterpret_cast<uint2*>(keys)[i] = make_uint2(lo, hi);
+        if (vals)
             reinterpret_cast<uint2*>(vals)[i] =
                 make_uint2(uint32_t(i << 1), uint32_t((i << 1) | 1u));  // contraction.hpp:16-18
-        }
         if (bitmap) {  // only the endpoints in this pass's slice [mark_lo, mark_hi]
             if (lo - mark_lo <= mark_hi - mark_lo) atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
             if (hi - mark_lo <= mark_hi - mark_lo) atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
         }
         lo_acc = lo < lo_acc ? lo : lo_acc;
         hi_acc = hi > hi_acc ? hi : hi_acc;
+      }
     }
     if (span) {
         const uint32_t wlo = __reduce_min_sync(kFull, lo_acc);
@@ -101,6 +122,7 @@ __global__ void __launch_bounds__(kThreads) k_unique(
     uint32_t* __restrict__ span, uint64_t* __restrict__ nb_out,
     uint32_t* __restrict__ err, uint64_t* __restrict__ status, uint32_t* __restrict__ ticket,
     const uint32_t* __restrict__ epoch_dev, uint32_t epoch_off) {
+    brmq::pdl_wait();
     const uint32_t epoch = *epoch_dev + epoch_off;
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_scan[kThreads / 32 + 1];
@@ -115,7 +137,7 @@ __global__ void __launch_bounds__(kThreads) k_unique(
         const uint4* v = reinterpret_cast<const uint4*>(pos + base);
 #pragma unroll
         for (int j = 0; j < kItems / 4; ++j) {
-            const uint4 x = __ldg(v + j);
+            const uint4 x = __ldcs(v + j);  // streamed: keeps cleft / cright in L2
             p[4 * j] = x.x; p[4 * j + 1] = x.y; p[4 * j + 2] = x.z; p[4 * j + 3] = x.w;
         }
     } else {
@@ -123,6 +145,13 @@ __global__ void __launch_bounds__(kThreads) k_unique(
         for (int j = 0; j < kItems; ++j) p[j] = base + j < m ? __ldg(pos + base + j) : 0u;
     }
     uint32_t prev = base > 0 && base - 1 < m ? __ldg(pos + base - 1) : 0u;
+    // the origins are loaded now: in flight during the look-back below
+    uint4 o4[kItems / 4];
+    if (base + kItems <= m && cleft) {
+        const uint4* v = reinterpret_cast<const uint4*>(org + base);
+#pragma unroll
+        for (int j = 0; j < kItems / 4; ++j) o4[j] = __ldcs(v + j);
+    }
     uint32_t heads = 0, cnt = 0;
     bool unsorted = false;
 #pragma unroll
@@ -158,12 +187,6 @@ __global__ void __launch_bounds__(kThreads) k_unique(
     }
     __syncthreads();
     uint64_t r = s_excl + excl;  // rank of the next head; item rank = r - 1 after its head
-    uint4 o4[kItems / 4];
-    if (base + kItems <= m && cleft) {
-        const uint4* v = reinterpret_cast<const uint4*>(org + base);
-#pragma unroll
-        for (int j = 0; j < kItems / 4; ++j) o4[j] = __ldg(v + j);
-    }
     const uint32_t* o = reinterpret_cast<const uint32_t*>(o4);
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
@@ -200,12 +223,72 @@ __global__ void __launch_bounds__(kThreads) k_unique(
     }
 }
 
+// ------------------------------------------------------------- mark sorted
+// Sorted endpoint positions -> the boundary bitmap (the dedup of
+// contraction.cpp:118-127: a position present any number of times is one bit).
+// Each thread walks 8 consecutive sorted positions and ORs the bits of a word
+// locally; a word strictly inside the thread's run is owned by it (plain
+// store: the bitmap is all-zero between solves), the first and last words may be
+// shared with the neighbours (atomicOr).  Checks the order (contraction.cpp:123)
+// and the range, and publishes the span.  The boundary ranks then come from the
+// bitmap (k_piece_count) and the query kernel's per-word ranks, as in the
+// bitmap pipeline: no look-back, no rank scatter.
+__global__ void __launch_bounds__(kThreads) k_mark_sorted(const uint32_t* __restrict__ pos, uint64_t m,
+                                                          uint64_t n, uint32_t* __restrict__ bitmap,
+                                                          uint32_t* __restrict__ span,
+                                                          uint32_t* __restrict__ err) {
+    brmq::pdl_wait();
+    const uint64_t base = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) * kItems;
+    if (base >= m) return;
+    uint32_t p[kItems];
+    if (base + kItems <= m) {
+        const uint4* v = reinterpret_cast<const uint4*>(pos + base);
+#pragma unroll
+        for (int j = 0; j < kItems / 4; ++j) {
+            const uint4 x = __ldcs(v + j);
+            p[4 * j] = x.x; p[4 * j + 1] = x.y; p[4 * j + 2] = x.z; p[4 * j + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) p[j] = base + j < m ? __ldg(pos + base + j) : 0u;
+    }
+    uint32_t prev = base > 0 ? __ldg(pos + base - 1) : 0u;
+    uint32_t bad = 0, word = 0xFFFFFFFFu, bits = 0;
+    bool first = true;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        if (base + j >= m) break;
+        const uint32_t x = p[j];
+        if (base + j > 0 && x < prev) bad |= 4u;  // contraction.cpp:123
+        prev = x;
+        if (x >= n) {
+            bad |= 2u;
+            continue;
+        }
+        if ((x >> 5) != word) {
+            if (bits) {
+                if (first) atomicOr(bitmap + word, bits);
+                else bitmap[word] = bits;
+                first = false;
+            }
+            word = x >> 5;
+            bits = 0;
+        }
+        bits |= 1u << (x & 31);
+    }
+    if (bits) atomicOr(bitmap + word, bits);
+    if (bad) atomicOr(err, bad);
+    if (base == 0) span[0] = ~p[0];
+    if (base + kItems >= m) span[1] = p[(m - 1 - base) < kItems ? (m - 1 - base) : 0];
+}
+
 // ------------------------------------------------------------ bitmap remap
 __global__ void __launch_bounds__(kThreads) k_remap_bitmap(const ulonglong2* __restrict__ Q,
                                                            uint64_t q, uint64_t n,
                                                            const uint2* __restrict__ word_info,
                                                            uint32_t* __restrict__ cleft,
                                                            uint32_t* __restrict__ cright_raw) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (i >= q) return;
     const ulonglong2 x = __ldg(Q + i);
@@ -220,6 +303,7 @@ __global__ void __launch_bounds__(kThreads) k_remap_bitmap(const ulonglong2* __r
 // --------------------------------------------------- stage-API helper kernels
 __global__ void k_split_eps(const uint2* __restrict__ eps, uint64_t m, uint32_t* __restrict__ keys,
                             uint32_t* __restrict__ vals) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < m) {
         const uint2 e = eps[i];
@@ -229,12 +313,14 @@ __global__ void k_split_eps(const uint2* __restrict__ eps, uint64_t m, uint32_t*
 }
 __global__ void k_join_eps(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                            uint64_t m, uint2* __restrict__ eps) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < m) eps[i] = make_uint2(keys[i], vals[i]);
 }
 __global__ void k_split_aq(const uint64_t* __restrict__ aq, const uint64_t* __restrict__ len,
                            uint64_t len_max, int32_t* __restrict__ values,
                            uint64_t* __restrict__ origin) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < len_max && i < *len) {
         values[i] = key_value(aq[i]);
@@ -243,6 +329,7 @@ __global__ void k_split_aq(const uint64_t* __restrict__ aq, const uint64_t* __re
 }
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, const uint64_t* __restrict__ len,
                              uint64_t len_max, uint64_t* __restrict__ out) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < len_max && i < *len) out[i] = a[i];
 }
@@ -252,6 +339,7 @@ __global__ void k_remap_search(const uint32_t* __restrict__ pos, const uint32_t*
                                uint64_t m, const uint64_t* __restrict__ boundary, uint64_t nb,
                                uint64_t q, uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
                                uint32_t* __restrict__ err) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const uint64_t p = pos[i];
@@ -269,6 +357,7 @@ __global__ void k_remap_search(const uint32_t* __restrict__ pos, const uint32_t*
 }
 __global__ void k_remap_finish(uint64_t q, const uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
                                uint8_t* __restrict__ dg) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= q) return;
     if (cr[i] == cl[i]) dg[i] = 1;  // contraction.cpp:191-197
@@ -282,6 +371,7 @@ __global__ void k_remap_queries(const ulonglong2* __restrict__ Q, uint64_t q,
                                 const uint64_t* __restrict__ boundary, uint64_t nb,
                                 uint32_t* __restrict__ cl, uint32_t* __restrict__ cr,
                                 uint8_t* __restrict__ dg, uint32_t* __restrict__ err) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= q) return;
     const ulonglong2 x = __ldg(Q + i);
@@ -311,6 +401,7 @@ __global__ void k_remap_queries(const ulonglong2* __restrict__ Q, uint64_t q,
     dg[i] = 0;
 }
 __global__ void k_keys_to_pos(uint64_t* __restrict__ t, uint64_t count) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < count) t[i] = t[i] == kNoKey ? ~0ull : uint64_t(key_pos(t[i]));
 }
@@ -324,6 +415,7 @@ __global__ void k_keys_to_pos(uint64_t* __restrict__ t, uint64_t count) {
 // entry: +inf) or all +inf (its first position).
 __global__ void k_marked_fill(const int32_t* __restrict__ A, const uint32_t* __restrict__ bnd,
                               const uint64_t* __restrict__ m_dev, uint64_t* __restrict__ E) {
+    brmq::pdl_wait();
     const uint64_t m = *m_dev;
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= m) return;
@@ -344,6 +436,7 @@ __global__ void k_marked_fill(const int32_t* __restrict__ A, const uint32_t* __r
 __global__ void k_marked_edges(const int32_t* __restrict__ A, uint64_t n,
                                const uint32_t* __restrict__ span, const uint64_t* __restrict__ m_dev,
                                uint64_t* __restrict__ E) {
+    brmq::pdl_wait();
     const uint32_t b0 = ~span[0], blast = span[1];
     if (b0 > blast) return;
     const uint64_t pre = b0, suf = n - 1 - blast;  // lengths
@@ -385,9 +478,9 @@ __global__ void k_query_st(const ulonglong2* __restrict__ Q, const uint32_t* __r
                            const uint32_t* __restrict__ cright_raw, uint64_t q,
                            const uint64_t* __restrict__ ST, uint64_t stride,
                            uint64_t* __restrict__ answers, const CtlPublish pub) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < q) st_one(Q, cleft, cright_raw, i, ST, stride, answers);
-    publish_control(pub);
 }
 
 inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
@@ -397,7 +490,8 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 // ------------------------------------------------------------------ launchers
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
-                   uint32_t* epoch_bump, uint32_t epoch_by) {
+                   uint32_t* epoch_bump, uint32_t epoch_by, uint64_t* fill0, uint64_t fill0_n,
+                   uint64_t* fill1, uint64_t fill1_n) {
     if (q == 0) return 0;
     // small batches: one CTA per SM (fewer span atomics, c2 -1.3 us); large ones
     // need the wide grid for the loads in flight (c5 at 148 CTAs: 0.25 -> 0.70 ms)
@@ -413,21 +507,33 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
     constexpr uint64_t kSliceBytes = uint64_t(32) << 20;
     const uint32_t slices = uint32_t((bm_bytes + kSliceBytes - 1) / kSliceBytes);
     if (slices <= 1) {
-        k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
-                                               bitmap, span, err, epoch_bump, epoch_by, 0u, ~0u);
+        brmq::launch_k(k_collect, dim3(grid), dim3(kThreads), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
+                                               bitmap, span, err, epoch_bump, epoch_by, 0u, ~0u,
+                                               fill0, fill0_n, fill1, fill1_n);
         return 1;
     }
     const uint64_t per = (n + slices - 1) / slices;
     for (uint32_t t = 0; t < slices; ++t) {
         const uint64_t a = t * per, b = (t + 1) * per < n ? (t + 1) * per : n;
-        k_collect<<<grid, kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
+        brmq::launch_k(k_collect, dim3(grid), dim3(kThreads), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
                                                bitmap, span, err, t == 0 ? epoch_bump : nullptr,
-                                               epoch_by, uint32_t(a), uint32_t(b - 1));
+                                               epoch_by, uint32_t(a), uint32_t(b - 1),
+                                               t == 0 ? fill0 : nullptr, t == 0 ? fill0_n : 0,
+                                               t == 0 ? fill1 : nullptr, t == 0 ? fill1_n : 0);
     }
     return int(slices);
 }
 
 size_t unique_status_words(uint64_t m) { return (m + kTile - 1) / kTile; }
+
+int launch_mark_sorted(const uint32_t* pos, uint64_t m, uint64_t n, uint32_t* bitmap, uint32_t* span,
+                       uint32_t* err, cudaStream_t s) {
+    if (m == 0) return 0;
+    const uint64_t threads = (m + kItems - 1) / kItems;
+    brmq::launch_k(k_mark_sorted, dim3(unsigned((threads + kThreads - 1) / kThreads)), dim3(kThreads), 0, s,
+                   pos, m, n, bitmap, span, err);
+    return 1;
+}
 
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n, uint32_t* boundary,
                   uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap, uint32_t* rfirst,
@@ -438,7 +544,7 @@ int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t
     uint32_t G = 0, R = 1;
     if (bitmap) contract_partition(n, &G, &R);
     if (bitmap && R != range_tiles) return -1;
-    k_unique<<<unsigned((m + kTile - 1) / kTile), kThreads, 0, s>>>(
+    brmq::launch_k(k_unique, dim3(unsigned((m + kTile - 1) / kTile)), dim3(kThreads), 0, s, 
         pos, org, m, n, boundary, cleft, cright_raw, bitmap, rfirst, R, G, span, nb_out, err,
         status, ticket, epoch_dev, epoch_off);
     return 1;
@@ -447,32 +553,32 @@ int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s) {
     if (q == 0) return 0;
-    k_remap_bitmap<<<g256(q), kThreads, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, n,
+    brmq::launch_k(k_remap_bitmap, dim3(g256(q)), dim3(kThreads), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, n,
                                                 word_info, cleft, cright_raw);
     return 1;
 }
 
 int launch_split_eps(const void* eps, uint64_t m, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
     if (!m) return 0;
-    k_split_eps<<<g256(m), 256, 0, s>>>(static_cast<const uint2*>(eps), m, keys, vals);
+    brmq::launch_k(k_split_eps, dim3(g256(m)), dim3(256), 0, s, static_cast<const uint2*>(eps), m, keys, vals);
     return 1;
 }
 int launch_join_eps(const uint32_t* keys, const uint32_t* vals, uint64_t m, void* eps,
                     cudaStream_t s) {
     if (!m) return 0;
-    k_join_eps<<<g256(m), 256, 0, s>>>(keys, vals, m, static_cast<uint2*>(eps));
+    brmq::launch_k(k_join_eps, dim3(g256(m)), dim3(256), 0, s, keys, vals, m, static_cast<uint2*>(eps));
     return 1;
 }
 int launch_split_aq(const uint64_t* aq, const uint64_t* len, uint64_t len_max, int32_t* values,
                     uint64_t* origin, cudaStream_t s) {
     if (!len_max) return 0;
-    k_split_aq<<<g256(len_max), 256, 0, s>>>(aq, len, len_max, values, origin);
+    brmq::launch_k(k_split_aq, dim3(g256(len_max)), dim3(256), 0, s, aq, len, len_max, values, origin);
     return 1;
 }
 int launch_u32_to_u64(const uint32_t* a, const uint64_t* len, uint64_t len_max, uint64_t* out,
                       cudaStream_t s) {
     if (!len_max) return 0;
-    k_u32_to_u64<<<g256(len_max), 256, 0, s>>>(a, len, len_max, out);
+    brmq::launch_k(k_u32_to_u64, dim3(g256(len_max)), dim3(256), 0, s, a, len, len_max, out);
     return 1;
 }
 int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
@@ -480,11 +586,11 @@ int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
                         uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s) {
     int l = 0;
     if (m) {
-        k_remap_search<<<g256(m), 256, 0, s>>>(pos, org, m, boundary, nb, q, cl, cr, err);
+        brmq::launch_k(k_remap_search, dim3(g256(m)), dim3(256), 0, s, pos, org, m, boundary, nb, q, cl, cr, err);
         ++l;
     }
     if (q) {
-        k_remap_finish<<<g256(q), 256, 0, s>>>(q, cl, cr, dg);
+        brmq::launch_k(k_remap_finish, dim3(g256(q)), dim3(256), 0, s, q, cl, cr, dg);
         ++l;
     }
     return l;
@@ -492,14 +598,14 @@ int launch_remap_search(const uint32_t* pos, const uint32_t* org, uint64_t m,
 int launch_remap_queries(const uint64_t* Q, uint64_t q, const uint64_t* boundary, uint64_t nb,
                          uint32_t* cl, uint32_t* cr, uint8_t* dg, uint32_t* err, cudaStream_t s) {
     if (!q) return 0;
-    k_remap_queries<<<g256(q), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), q, boundary, nb,
+    brmq::launch_k(k_remap_queries, dim3(g256(q)), dim3(256), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, boundary, nb,
                                              cl, cr, dg, err);
     return 1;
 }
 int launch_marked_fill(const int32_t* A, const uint32_t* boundary, const uint64_t* m_dev,
                        uint64_t m_max, uint64_t* E, cudaStream_t s) {
     if (!m_max) return 0;
-    k_marked_fill<<<g256(m_max), 256, 0, s>>>(A, boundary, m_dev, E);
+    brmq::launch_k(k_marked_fill, dim3(g256(m_max)), dim3(256), 0, s, A, boundary, m_dev, E);
     return 1;
 }
 
@@ -507,7 +613,7 @@ int launch_marked_edges(const int32_t* A, uint64_t n, const uint32_t* span, cons
                         uint64_t* E, cudaStream_t s) {
     if (!n) return 0;
     const uint64_t g = (n + 255) / 256;
-    k_marked_edges<<<unsigned(g < 148 * 8 ? g : 148 * 8), 256, 0, s>>>(A, n, span, m_dev, E);
+    brmq::launch_k(k_marked_edges, dim3(unsigned(g < 148 * 8 ? g : 148 * 8)), dim3(256), 0, s, A, n, span, m_dev, E);
     return 1;
 }
 
@@ -515,14 +621,14 @@ int launch_query_st(const uint64_t* Q, const uint32_t* cleft, const uint32_t* cr
                     uint64_t q, const uint64_t* ST, uint64_t stride, uint64_t* answers,
                     cudaStream_t s, const CtlPublish& pub) {
     if (!q) return 0;
-    k_query_st<<<g256(q), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(Q), cleft, cright_raw,
+    brmq::launch_k(k_query_st, dim3(g256(q)), dim3(256), 0, s, reinterpret_cast<const ulonglong2*>(Q), cleft, cright_raw,
                                         q, ST, stride, answers, pub);
     return 1;
 }
 
 int launch_keys_to_pos(uint64_t* t, uint64_t count, cudaStream_t s) {
     if (!count) return 0;
-    k_keys_to_pos<<<g256(count), 256, 0, s>>>(t, count);
+    brmq::launch_k(k_keys_to_pos, dim3(g256(count)), dim3(256), 0, s, t, count);
     return 1;
 }
 

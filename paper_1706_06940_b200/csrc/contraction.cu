@@ -95,6 +95,30 @@ __device__ __forceinline__ uint64_t aq_slot(uint64_t idx) {
     return MARKED ? 2 * idx + 2 : idx;
 }
 
+// Where a closed area goes.  FUSE (BbST_CON with a small A_Q): besides the
+// store, its key is folded into the 32-key run minima (`sub`) and the k-block
+// minima (row 0 of the block Sparse Table) with fire-and-forget reductions, so
+// no block-argmin pass over A_Q follows (measured at c2: +4 us in the
+// contraction for -7.5 us of block-argmin launch; a last-CTA build of the
+// table's upper rows inside the contraction cost +8 us, rejected).
+struct AqOut {
+    uint64_t* aq;
+    uint64_t* sub;
+    uint64_t* blk;
+    uint32_t kshift;
+};
+__device__ __forceinline__ void red_min_u64(uint64_t* p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool MARKED, bool FUSE>
+__device__ __forceinline__ void put_area(const AqOut& o, uint64_t idx, uint64_t key) {
+    o.aq[aq_slot<MARKED>(idx)] = key;
+    if constexpr (FUSE && !MARKED) {
+        red_min_u64(o.sub + (idx >> 5), key);
+        red_min_u64(o.blk + (idx >> o.kshift), key);
+    }
+}
+
 __device__ __forceinline__ int32_t comp(const int4& x, int e) {
     return e == 0 ? x.x : e == 1 ? x.y : e == 2 ? x.z : x.w;
 }
@@ -141,9 +165,9 @@ __device__ __forceinline__ uint64_t row_min(const RW& rw, uint32_t r, int lo, in
 // closes area `rank`, ...); hp = min over [lo, first boundary] (the part of the
 // area the row's first boundary closes, completed after the warp scan), run =
 // min over [last boundary, hi] (the open segment the row hands on).
-template <bool MARKED, class RW>
+template <bool MARKED, bool FUSE, class RW>
 __device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, int lo, int hi,
-                                         uint64_t rank, uint64_t* __restrict__ aq, uint64_t& hp,
+                                         uint64_t rank, const AqOut& aq, uint64_t& hp,
                                          uint64_t& run) {
     int32_t rv = 0x7FFFFFFF;
     int ri = -1;
@@ -161,7 +185,7 @@ __device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, 
                 uint64_t k = pack_key(v, uint32_t(rw.pos(r, j)));  // inclusive right end
                 if (ri >= 0) k = kmin(k, pack_key(rv, uint32_t(rw.pos(r, ri))));
                 if (seen) {
-                    aq[aq_slot<MARKED>(rank)] = k;
+                    put_area<MARKED, FUSE>(aq, rank, k);
                     ++rank;
                 } else {
                     hp = k;
@@ -183,9 +207,9 @@ __device__ __forceinline__ void row_pass(const RW& rw, uint32_t r, uint32_t fl, 
 // `run`, so the unflagged lanes do their row minimum in the same instruction
 // stream instead of a separate, serialised row_min pass; element 0 is peeled
 // (the run is never empty after it).
-template <bool MARKED, class RW>
+template <bool MARKED, bool FUSE, class RW>
 __device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t fl, uint64_t rank,
-                                             uint64_t* __restrict__ aq, uint64_t& hp,
+                                             const AqOut& aq, uint64_t& hp,
                                              uint64_t& run) {
     const uint32_t p0 = uint32_t(rw.pos(r, 0));
     int4 x = rw.chunk(r, 0);
@@ -203,7 +227,7 @@ __device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t 
             if ((fl >> j) & 1u) {
                 const uint64_t k = v < rv ? pack_key(v, p0 + j) : pack_key(rv, p0 + ri);
                 if (seen) {
-                    aq[aq_slot<MARKED>(rank)] = k;
+                    put_area<MARKED, FUSE>(aq, rank, k);
                     ++rank;
                 } else {
                     hp = k;
@@ -231,9 +255,9 @@ __device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t 
 // element (BSSY/BRA/BSYNC around every compare), this one 8.
 constexpr int kCap = 16;  // capture slots per lane
 constexpr size_t kCapSmem = size_t(NW) * kCap * 32 * 8;  // dynamic shared memory of k_contract
-template <bool MARKED, class RW>
+template <bool MARKED, bool FUSE, class RW>
 __device__ __forceinline__ void row_pass_cap(const RW& rw, uint32_t r, uint32_t fl, uint64_t rank,
-                                             uint64_t* __restrict__ aq, uint64_t& hp, uint64_t& run,
+                                             const AqOut& aq, uint64_t& hp, uint64_t& run,
                                              uint32_t cap /* shared address of slot 0 of this lane */) {
     const uint32_t p0 = uint32_t(rw.pos(r, 0));
     int32_t rv = 0x7FFFFFFF;
@@ -265,7 +289,7 @@ __device__ __forceinline__ void row_pass_cap(const RW& rw, uint32_t r, uint32_t 
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cv), "=r"(ci) : "r"(cap + i * 32u * 8u) : "memory");
         const uint64_t k = pack_key(int32_t(cv), p0 + ci);
         if (i == 0) hp = k;
-        else aq[aq_slot<MARKED>(rank + i - 1)] = k;
+        else put_area<MARKED, FUSE>(aq, rank + i - 1, k);
     }
 }
 
@@ -295,6 +319,8 @@ __global__ void __launch_bounds__(NT) k_piece_count(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ span, uint64_t R,
                                                     uint32_t* __restrict__ pcnt,
                                                     uint32_t* __restrict__ rcnt) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     __shared__ uint32_t s_c[NW];
     const uint32_t b0 = ~span[0], blast = span[1];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -343,6 +369,14 @@ struct ContractArgs {
     const uint32_t* pcnt;  // nullable: [G * NW] boundaries per piece (k_piece_count)
     const uint32_t* epoch_dev;  // device epoch counter (bumped once per solve)
     uint32_t epoch_off;
+    // FUSE instances: 32-key run minima and row 0 of the k-block Sparse Table
+    // over A_Q (filled by reductions), its row stride, log2(k), and b_dev =
+    // ceil(|A_Q| / k)
+    uint64_t* fuse_sub;
+    uint64_t* fuse_st;
+    uint64_t fuse_stride;
+    uint32_t fuse_kshift;
+    uint64_t* b_dev;
 };
 
 // MARKED: ST-RMQ_CON's marked contraction -- marked positions read as +inf
@@ -350,8 +384,9 @@ struct ContractArgs {
 // SPARSE = false: every warp tile holding a boundary takes the dense one-pass
 // rows (the instance for high boundary densities: without the sparse path
 // compiled in, c5-con's contraction runs 5% faster).
-template <bool VEC, bool MARKED, bool SPARSE = true>
-__global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
+template <bool VEC, bool MARKED, bool SPARSE, bool FUSE>
+__device__ __forceinline__ void contract_body(const ContractArgs& c) {
+    const AqOut out{c.aq, c.fuse_sub, c.fuse_st, c.fuse_kshift};
     __shared__ __align__(128) int4 s_rows[NW][kWTile / 4];  // per warp: 32 rows x 128 B, swizzled
     extern __shared__ __align__(16) uint2 s_cap[];  // [NW][kCap][32] boundary captures (dense rows)
     __shared__ uint32_t s_cnt[NW];
@@ -460,6 +495,7 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
                 for (int w = 0; w < NW; ++w) nb += s_cnt[w];
                 *c.nb_out = nb;
                 *c.aq_len = MARKED ? 2 * nb + 1 : nb - 1;
+                if (FUSE) *c.b_dev = (nb - 1 + (1u << c.fuse_kshift) - 1) >> c.fuse_kshift;
             }
         }
         __syncthreads();
@@ -549,12 +585,12 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
             uint64_t hp = kNoKey;
             if (!GEN) {
                 if (!__any_sync(kFull, __popc(fl) > kCap))
-                    row_pass_cap<MARKED>(rs, lane, fl, rank, c.aq, hp, run,
+                    row_pass_cap<MARKED, FUSE>(rs, lane, fl, rank, out, hp, run,
                                          smem_u32(s_cap) + (warp * kCap * 32u + lane) * 8u);
                 else
-                    row_pass_all<MARKED>(rs, lane, fl, rank, c.aq, hp, run);
+                    row_pass_all<MARKED, FUSE>(rs, lane, fl, rank, out, hp, run);
             }
-            else if (any && fl) row_pass<MARKED>(rs, lane, fl, jlo, jhi, rank, c.aq, hp, run);
+            else if (any && fl) row_pass<MARKED, FUSE>(rs, lane, fl, jlo, jhi, rank, out, hp, run);
             SegMin inc{run, cntb != 0};
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -574,7 +610,7 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
                 my_rank = rank;
                 const uint64_t first = kmin(in.k, hp);   // the area the row's first boundary closes
                 if (in.f) {
-                    c.aq[aq_slot<MARKED>(rank - 1)] = first;
+                    put_area<MARKED, FUSE>(out, rank - 1, first);
                 } else {  // first boundary of the piece: its area opened in an earlier piece
                     head = first;
                     head_set = true;
@@ -613,7 +649,7 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
                             head = val;
                             head_set = true;
                         } else {
-                            c.aq[aq_slot<MARKED>(rank - 1)] = val;
+                            put_area<MARKED, FUSE>(out, rank - 1, val);
                         }
                     }
                     continue;
@@ -644,7 +680,7 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
                         head = val;
                         head_set = true;
                     } else if (rk > 0) {
-                        c.aq[aq_slot<MARKED>(rk - 1)] = val;
+                        put_area<MARKED, FUSE>(out, rk - 1, val);
                     }
                 }
             }
@@ -718,7 +754,14 @@ __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __gri
             p -= 32;
         }
     }
-    if (lane == 0) c.aq[aq_slot<MARKED>(rank_first - 1)] = kmin(acc, s_head[warp]);
+    if (lane == 0) put_area<MARKED, FUSE>(out, rank_first - 1, kmin(acc, s_head[warp]));
+}
+
+template <bool VEC, bool MARKED, bool SPARSE = true, bool FUSE = false>
+__global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
+    contract_body<VEC, MARKED, SPARSE, FUSE>(c);
 }
 
 int contract_grid() {
@@ -733,6 +776,8 @@ int contract_grid() {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const void* fns[] = {reinterpret_cast<const void*>(k_contract<true, false>),
                              reinterpret_cast<const void*>(k_contract<true, false, false>),
+                             reinterpret_cast<const void*>(k_contract<true, false, true, true>),
+                             reinterpret_cast<const void*>(k_contract<true, false, false, true>),
                              reinterpret_cast<const void*>(k_contract<true, true>),
                              reinterpret_cast<const void*>(k_contract<true, true, false>),
                              reinterpret_cast<const void*>(k_contract<false, false>),
@@ -759,7 +804,7 @@ int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n,
                        uint32_t* rcnt, cudaStream_t s) {
     uint32_t G = 0, R = 0;
     contract_partition(n, &G, &R);
-    k_piece_count<<<G, NT, 0, s>>>(bitmap, span, R, pcnt, rcnt);
+    brmq::launch_k(k_piece_count, dim3(G), dim3(NT), 0, s, bitmap, span, R, pcnt, rcnt);
     return 1;
 }
 
@@ -778,25 +823,54 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     uint64_t* aq_len,
                     uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
                     uint32_t epoch_off, cudaStream_t s, bool marked, const uint32_t* pcnt,
-                    uint64_t endpoints) {
+                    uint64_t endpoints, const ContractFuse* fuse, bool* fused) {
+    if (fused) *fused = false;
     if (n == 0) return 0;
     uint32_t G = 0, R = 0;
     contract_partition(n, &G, &R);
+    const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
+    // the fused block minima + table tail (small A_Q: the caller filled sub and
+    // the table's row 0 with kNoKey)
+    const bool fz = fuse && vec && !marked;
     ContractArgs args{A, n, bitmap, span, aq, nb_out, aq_len, word_info, rcnt, R,
                       prefix ? 1u : 0u, status, status + kMaxContractRanges, pcnt, epoch_dev,
-                      epoch_off};
+                      epoch_off, fz ? fuse->sub : nullptr, fz ? fuse->st : nullptr,
+                      fz ? fuse->b_max : 0, fz ? fuse->kshift : 0u, fz ? fuse->b_dev : nullptr};
     void* params[] = {&args};
-    const bool vec = (reinterpret_cast<uintptr_t>(A) & 15u) == 0;
     // >= 8 endpoints per 1024 positions on average: nearly every flagged warp tile
     // has more than kDense flagged rows, so the dense-only instance runs
     const bool dense = endpoints >= uint64_t(kDenseEndpoints) * (n / kWTile + 1);
     const void* fn = vec ? (marked ? (dense ? reinterpret_cast<const void*>(k_contract<true, true, false>)
                                             : reinterpret_cast<const void*>(k_contract<true, true>))
+                                   : fz ? (dense ? reinterpret_cast<const void*>(k_contract<true, false, false, true>)
+                                                 : reinterpret_cast<const void*>(k_contract<true, false, true, true>))
                                    : (dense ? reinterpret_cast<const void*>(k_contract<true, false, false>)
                                             : reinterpret_cast<const void*>(k_contract<true, false>)))
                          : (marked ? reinterpret_cast<const void*>(k_contract<false, true>)
                                    : reinterpret_cast<const void*>(k_contract<false, false>));
-    cudaLaunchCooperativeKernel(fn, dim3(G), dim3(NT), params, kCapSmem, s);
+    if (fused) *fused = fz;
+    // cooperative (co-residency checked); inside a solve also a PDL secondary: its
+    // CTAs are placed as the predecessor's retire and wait in pdl_wait, and the
+    // predecessor never waits on them, so co-residency is reached before any
+    // cross-CTA wait begins
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = kCapSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PdlState& st = pdl_state();
+    if (st.on && !st.first) {
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs = 2;
+    }
+    st.first = false;
+    cudaLaunchKernelExC(&cfg, fn, params);
     return 1;  // launch errors surface through the caller's cudaGetLastError
 }
 

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -128,8 +129,11 @@ int brmq_account_memory(int algo, uint64_t n, uint64_t q, const uint32_t* ks, ui
             b = 8 * block_cells(n, ks[h - 1]);
             break;
         case BRMQ_ALGO_BBST_ML:
+            // the structures the chain solve allocates (api.cu solve_chain): the
+            // Sparse Table over the k_h-blocks plus one 8-byte key per k_j-block of
+            // every lower level j < h - 1
             b = 8 * block_cells(n, ks[h - 1]);
-            if (h >= 2) b += 8 * ((n + ks[0] - 1) / ks[0]);
+            for (uint32_t j = 0; j + 1 < h; ++j) b += 8 * ((n + ks[j] - 1) / ks[j]);
             break;
         default:
             return set_error(BRMQ_EINVAL, "unknown algorithm id");
@@ -240,6 +244,104 @@ int brmq_verify_answers(const int32_t* A, uint64_t n, const brmq_query* Q, uint6
         *bad += nbad[w];
         *first_bad = std::min(*first_bad, fbad[w]);
     }
+    return BRMQ_OK;
+}
+
+// ---- emit_plot
+int brmq_emit_plot(const char* csv_path, const char* svg_path) {
+    if (!csv_path || !svg_path) return set_error(BRMQ_EINVAL, "null path");
+    FILE* f = fopen(csv_path, "rb");
+    if (!f) return set_error(BRMQ_EIO, "emit_plot: cannot read the CSV");
+    std::string text;
+    char buf[4096];
+    for (size_t r; (r = fread(buf, 1, sizeof(buf), f)) > 0;) text.append(buf, r);
+    fclose(f);
+    // columns of emit_csv: algo, n, q, k_chain, ..., t_total_ns (index 10)
+    struct Pt { double q, t; };
+    std::map<std::string, std::vector<Pt>> series;  // ordered: deterministic output
+    uint64_t n0 = 0;
+    bool first = true, header = true;
+    size_t pos = 0;
+    while (pos < text.size()) {
+        size_t e = text.find('\n', pos);
+        if (e == std::string::npos) e = text.size();
+        std::string line = text.substr(pos, e - pos);
+        pos = e + 1;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (line.empty()) continue;
+        if (header) {  // the header row
+            header = false;
+            if (line.compare(0, 5, "algo,") == 0) continue;
+        }
+        std::vector<std::string> col;
+        for (size_t a = 0;;) {
+            const size_t b = line.find(',', a);
+            col.push_back(line.substr(a, b == std::string::npos ? std::string::npos : b - a));
+            if (b == std::string::npos) break;
+            a = b + 1;
+        }
+        if (col.size() < 11) return set_error(BRMQ_EINVAL, "emit_plot: malformed CSV row");
+        const uint64_t n = strtoull(col[1].c_str(), nullptr, 10);
+        if (first) n0 = n;
+        else if (n != n0) return set_error(BRMQ_EINVAL, "emit_plot: records do not share n");
+        first = false;
+        const double q = strtod(col[2].c_str(), nullptr), t = strtod(col[10].c_str(), nullptr);
+        if (q > 0 && t > 0) series[col[0] + (col[3].empty() ? "" : " k=" + col[3])].push_back({q, t});
+    }
+    if (series.empty()) {
+        fprintf(stderr, "brmq: emit_plot: no records, nothing written\n");
+        return BRMQ_OK;
+    }
+    double qlo = 1e300, qhi = 0, tlo = 1e300, thi = 0;
+    for (auto& kv : series) {
+        std::sort(kv.second.begin(), kv.second.end(), [](const Pt& a, const Pt& b) { return a.q < b.q; });
+        for (const Pt& p : kv.second) {
+            qlo = std::min(qlo, p.q); qhi = std::max(qhi, p.q);
+            tlo = std::min(tlo, p.t); thi = std::max(thi, p.t);
+        }
+    }
+    const double lq0 = std::floor(std::log10(qlo)), lq1 = std::max(lq0 + 1, std::ceil(std::log10(qhi)));
+    const double lt0 = std::floor(std::log10(tlo)), lt1 = std::max(lt0 + 1, std::ceil(std::log10(thi)));
+    const double W = 720, H = 480, L = 80, R = 220, T = 30, B = 60;
+    auto X = [&](double q) { return L + (std::log10(q) - lq0) / (lq1 - lq0) * (W - L - R); };
+    auto Y = [&](double t) { return H - B - (std::log10(t) - lt0) / (lt1 - lt0) * (H - T - B); };
+    FILE* o = fopen(svg_path, "wb");
+    if (!o) return set_error(BRMQ_EIO, "emit_plot: cannot write the SVG");
+    fprintf(o, "<svg xmlns=\"http://www.w3.org/2000/svg\" width=\"%.0f\" height=\"%.0f\" "
+               "font-family=\"sans-serif\" font-size=\"12\">\n", W, H);
+    fprintf(o, "<rect width=\"100%%\" height=\"100%%\" fill=\"white\"/>\n");
+    fprintf(o, "<text x=\"%.0f\" y=\"18\">batched RMQ, n = %llu: total time vs q</text>\n", L,
+            (unsigned long long)n0);
+    for (double d = lq0; d <= lq1 + 1e-9; d += 1) {
+        fprintf(o, "<line x1=\"%.1f\" y1=\"%.1f\" x2=\"%.1f\" y2=\"%.1f\" stroke=\"#ddd\"/>\n", X(std::pow(10, d)), T,
+                X(std::pow(10, d)), H - B);
+        fprintf(o, "<text x=\"%.1f\" y=\"%.1f\" text-anchor=\"middle\">1e%.0f</text>\n", X(std::pow(10, d)),
+                H - B + 16, d);
+    }
+    for (double d = lt0; d <= lt1 + 1e-9; d += 1) {
+        fprintf(o, "<line x1=\"%.1f\" y1=\"%.1f\" x2=\"%.1f\" y2=\"%.1f\" stroke=\"#ddd\"/>\n", L, Y(std::pow(10, d)),
+                W - R, Y(std::pow(10, d)));
+        fprintf(o, "<text x=\"%.1f\" y=\"%.1f\" text-anchor=\"end\">1e%.0f ns</text>\n", L - 6,
+                Y(std::pow(10, d)) + 4, d);
+    }
+    fprintf(o, "<text x=\"%.1f\" y=\"%.1f\" text-anchor=\"middle\">q (log scale)</text>\n", (L + W - R) / 2,
+            H - 16);
+    static const char* kColors[] = {"#1f77b4", "#d62728", "#2ca02c", "#9467bd", "#ff7f0e", "#8c564b",
+                                    "#e377c2", "#17becf"};
+    int si = 0;
+    for (const auto& kv : series) {
+        const char* c = kColors[si % 8];
+        fprintf(o, "<polyline class=\"series\" fill=\"none\" stroke=\"%s\" stroke-width=\"2\" points=\"", c);
+        for (const Pt& p : kv.second) fprintf(o, "%.1f,%.1f ", X(p.q), Y(p.t));
+        fprintf(o, "\"/>\n");
+        for (const Pt& p : kv.second)
+            fprintf(o, "<circle cx=\"%.1f\" cy=\"%.1f\" r=\"3\" fill=\"%s\"/>\n", X(p.q), Y(p.t), c);
+        fprintf(o, "<text x=\"%.1f\" y=\"%.1f\" fill=\"%s\">%s</text>\n", W - R + 12, T + 16 + 18.0 * si, c,
+                kv.first.c_str());
+        ++si;
+    }
+    fprintf(o, "</svg>\n");
+    fclose(o);
     return BRMQ_OK;
 }
 

@@ -10,8 +10,59 @@
 
 namespace brmq {
 
-// End-of-solve publication of the control header into host-mapped memory by the
-// last CTA of the final kernel (common.cuh publish_control); host == nullptr: off.
+// ---------------------------------------------------------------- launches
+// Programmatic dependent launch (PDL) inside a solve: every kernel after the
+// solve's first is launched with programmatic stream serialization, so its CTAs
+// are scheduled while its predecessor drains (launch latency and the
+// predecessor's tail overlap); each kernel opens with griddepcontrol.wait
+// (common.cuh pdl_wait), which returns once the predecessor grid has completed
+// and its memory is visible -- so the data dependences are unchanged, and since
+// every kernel waits before it can complete, completion stays transitive along
+// the chain.  Outside a PdlScope (stage entry points, timed stages) launches
+// are plain stream-ordered launches.
+struct PdlState {
+    bool on = false;
+    bool first = true;
+};
+inline PdlState& pdl_state() {
+    static thread_local PdlState st;
+    return st;
+}
+struct PdlScope {
+    explicit PdlScope(bool on) { pdl_state() = PdlState{on, true}; }
+    ~PdlScope() { pdl_state() = PdlState{}; }
+    PdlScope(const PdlScope&) = delete;
+    PdlScope& operator=(const PdlScope&) = delete;
+};
+// A kernel launch on `s`; launch errors surface through cudaGetLastError.
+template <class... P, class... A>
+inline void launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    PdlState& st = pdl_state();
+    if (st.on && !st.first) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    st.first = false;
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<A&&>(args)...) != cudaSuccess) {
+        // leave the error for the caller's cudaGetLastError (not consumed here)
+    }
+}
+// A plain (non-PDL) launch point inside a scope: the next kernel after it is
+// launched normally too (e.g. after a memcpy or an event record).
+inline void pdl_break() { pdl_state().first = true; }
+
+// End-of-solve publication of the control header into host-mapped memory: done
+// by api.cu's k_publish after the final kernel (the kernels' `pub` arguments are
+// unused since; kept so the launcher signatures stay stable).
 struct CtlPublish {
     const uint32_t* ctl;  // device control header (u32 words)
     uint32_t* host;       // host-mapped mirror
@@ -104,9 +155,13 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
 constexpr uint32_t kMaxContractRanges = 2048;
 constexpr int kContractTileLog2 = 12;  // 4096-position tiles
 void contract_partition(uint64_t n, uint32_t* G, uint32_t* R);
+// fill0 / fill1 (nullable): ranges set to kNoKey on the way (ContractFuse's sub
+// and table row 0)
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
-                   uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0);
+                   uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0,
+                   uint64_t* fill0 = nullptr, uint64_t fill0_n = 0, uint64_t* fill1 = nullptr,
+                   uint64_t fill1_n = 0);
 // Boundaries per contraction piece (pcnt[g * 8 + w], 8 warps per range) and per
 // range (rcnt[g]), popcounted from the bitmap.
 #ifndef BRMQ_CWARPS
@@ -116,6 +171,10 @@ constexpr uint32_t kContractWarps = BRMQ_CWARPS;
 int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* pcnt,
                        uint32_t* rcnt, cudaStream_t s);
 size_t unique_status_words(uint64_t m);
+// Sorted endpoint positions -> boundary bitmap + span (+ err bits 2: range, 4:
+// unsorted); the ranks then come from the bitmap (launch_piece_count).
+int launch_mark_sorted(const uint32_t* pos, uint64_t m, uint64_t n, uint32_t* bitmap, uint32_t* span,
+                       uint32_t* err, cudaStream_t s);
 int launch_unique(const uint32_t* pos, const uint32_t* org, uint64_t m, uint64_t n,
                   uint32_t* boundary, uint32_t* cleft, uint32_t* cright_raw, uint32_t* bitmap,
                   uint32_t* rcnt, uint32_t range_tiles, uint32_t* span, uint64_t* nb_out, uint32_t* err, uint64_t* status,
@@ -126,11 +185,23 @@ size_t contract_status_words();    // status-arena words the contraction needs
 // Persistent cooperative contraction (contract.cu): bitmap of boundaries ->
 // packed A_Q keys, |boundary| (nb_out) and |A_Q|; word_info (nullable) gets
 // (rank prefix, bits) of every non-empty bitmap word, which is cleared.
+// Small A_Q (BbST_CON, power-of-two k in [64, 512]): the contraction also
+// yields the 32-key run minima (sub) and row 0 of the block Sparse Table (st) by
+// reductions, and stores b = ceil(|A_Q| / k) in *b_dev.  sub[0 .. ceil(aq_max /
+// 32)) and st[0 .. b_max) must hold kNoKey beforehand (k_collect fills them).
+struct ContractFuse {
+    uint64_t* sub;
+    uint64_t* st;
+    uint64_t b_max;
+    uint32_t kshift;
+    uint64_t* b_dev;
+};
 int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32_t* span,
                     const uint32_t* rcnt, bool prefix, uint64_t* aq, uint64_t* nb_out, uint64_t* aq_len, uint2* word_info,
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
                     cudaStream_t s, bool marked = false,
-                    const uint32_t* pcnt = nullptr, uint64_t endpoints = 0);
+                    const uint32_t* pcnt = nullptr, uint64_t endpoints = 0,
+                    const ContractFuse* fuse = nullptr, bool* fused = nullptr);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)

@@ -27,6 +27,8 @@
 // for BbST_CON.  For A_Q, "stored min lies inside the range" is decided on
 // original positions: aq_origin is non-decreasing, so a block-min
 // key whose origin is >= l (resp. <= r) is present in the partial range.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -68,17 +70,6 @@ struct ElemI32 {
         if (v * 4 + 1 < len) x.y = __ldg(data + v * 4 + 1);
         if (v * 4 + 2 < len) x.z = __ldg(data + v * 4 + 2);
         return x;
-    }
-    // min key over the elements of vector v that lie in [lo, hi]
-    __device__ __forceinline__ uint64_t vec_min(const vec_t& x, uint64_t v, uint64_t lo,
-                                                uint64_t hi) const {
-        const uint64_t p = v * 4;
-        uint64_t b = kNoKey;
-        if (p + 0 >= lo && p + 0 <= hi) b = kmin(b, pack_key(x.x, uint32_t(p + 0)));
-        if (p + 1 >= lo && p + 1 <= hi) b = kmin(b, pack_key(x.y, uint32_t(p + 1)));
-        if (p + 2 >= lo && p + 2 <= hi) b = kmin(b, pack_key(x.z, uint32_t(p + 2)));
-        if (p + 3 >= lo && p + 3 <= hi) b = kmin(b, pack_key(x.w, uint32_t(p + 3)));
-        return b;
     }
     // Lane accumulator over the lane's vectors in increasing position order: a
     // value and its position in 32-bit registers (strict '<' keeps the leftmost),
@@ -191,6 +182,79 @@ struct QueryContractedWI {
     }
 };
 
+// L2 prefetch of the 16-byte vectors [v0, v0 + nv) of A (one bulk request per
+// range, issued by the lane that owns the query as soon as it knows the range
+// must be scanned): the warp's serial scan rounds then hit L2 (~250 cycles)
+// instead of DRAM, and all of a warp's ranges are fetched concurrently.
+__device__ __forceinline__ void prefetch_vecs_l2(const int32_t* A, uint64_t v0, uint32_t nv) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A + 4 * v0), "r"(nv * 16u)
+                 : "memory");
+}
+
+// Masked minimum of one 16-byte vector: elements t in [a, b] only (a vector of
+// the range always holds at least one of them).
+__device__ __forceinline__ int32_t vec_min_masked(const int4& x, uint32_t a, uint32_t b) {
+    const int32_t m0 = a == 0u ? x.x : 0x7FFFFFFF;
+    const int32_t m1 = (a <= 1u && b >= 1u) ? x.y : 0x7FFFFFFF;
+    const int32_t m2 = (a <= 2u && b >= 2u) ? x.z : 0x7FFFFFFF;
+    const int32_t m3 = b == 3u ? x.w : 0x7FFFFFFF;
+    return __vimin3_s32(m0, m1, min(m2, m3));
+}
+// First element t in [a, b] of the vector equal to wv (one exists).
+__device__ __forceinline__ uint32_t vec_first_eq(const int4& x, uint32_t a, uint32_t b, int32_t wv) {
+    return (a == 0u && x.x == wv) ? 0u : (a <= 1u && b >= 1u && x.y == wv) ? 1u
+                                       : (a <= 2u && b >= 2u && x.z == wv) ? 2u : 3u;
+}
+
+// Leftmost-min key of A[lo..hi] (within one block, 16-byte aligned A), by the
+// whole warp.  Value pass: lane j takes the range's vectors j, j + 32, ...
+// (NJ per lane, coalesced), masked 3-way mins, one redux.min; position pass:
+// each lane's first vector holding the minimum gives its first element equal to
+// it, and one redux.min over the element offsets is the leftmost position.
+// ~30 instructions per lane for a range of <= 32 vectors (NJ = 1), against ~90
+// for the per-element (value, position) accumulator it replaces (ncu: the c3
+// h = 1 query kernel was issue-bound, 69% of issue slots busy).
+template <int NJ>
+__device__ __forceinline__ uint64_t scan_i32_vecs(const ElemI32& e, uint64_t v0, uint32_t nv,
+                                                  uint32_t lo_t, uint32_t hi_t) {
+    const uint32_t lane = lane_id();
+    int4 x[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const uint32_t vi = lane + 32u * j;
+        x[j] = vi < nv ? e.load_vec(v0 + vi) : make_int4(0, 0, 0, 0);
+    }
+    int32_t m[NJ];
+    int32_t lm = 0x7FFFFFFF;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const uint32_t vi = lane + 32u * j;
+        const uint32_t a = vi == 0u ? lo_t : 0u, b = vi == nv - 1u ? hi_t : 3u;
+        m[j] = vi < nv ? vec_min_masked(x[j], a, b) : 0x7FFFFFFF;
+        lm = min(lm, m[j]);
+    }
+    const int32_t wv = __reduce_min_sync(kFull, lm);
+    uint32_t cand = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = NJ - 1; j >= 0; --j) {  // the lane's first vector holding wv wins
+        const uint32_t vi = lane + 32u * j;
+        if (vi < nv && m[j] == wv) {
+            const uint32_t a = vi == 0u ? lo_t : 0u, b = vi == nv - 1u ? hi_t : 3u;
+            cand = 4u * vi + vec_first_eq(x[j], a, b, wv);
+        }
+    }
+    const uint32_t off = __reduce_min_sync(kFull, cand);
+    return pack_key(wv, uint32_t(4 * v0) + off);
+}
+
+template <int VPL>
+__device__ __forceinline__ uint64_t scan_i32(const ElemI32& e, uint32_t lo, uint32_t hi) {
+    const uint64_t v0 = lo >> 2;
+    const uint32_t nv = (hi >> 2) - (lo >> 2) + 1u;
+    if (VPL <= 1 || nv <= 32u) return scan_i32_vecs<1>(e, v0, nv, lo & 3u, hi & 3u);
+    return scan_i32_vecs<(VPL > 1 ? VPL : 1)>(e, v0, nv, lo & 3u, hi & 3u);
+}
+
 template <class E>
 __device__ __forceinline__ uint64_t scan_generic(const E& e, uint64_t lo, uint64_t hi) {
     uint64_t b = kNoKey;
@@ -247,8 +311,97 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
         }
     }
 
+    if constexpr (std::is_same<E, ElemI32>::value && VPL > 0) {
+        // a range inside at most two 16-byte vectors (<= 8 cells) is scanned by its
+        // own lane at once: no warp round for it (c3: ~1 in 10 queries)
+        auto tiny = [&](bool& t, uint64_t lo, uint64_t hi) {
+            if (!t || (hi >> 2) - (lo >> 2) > 1) return;
+            t = false;
+            const uint64_t v0 = lo >> 2;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint64_t v = v0 + u;
+                if (v * 4 > hi) break;
+                const int4 x = elem.load_vec(v);
+                const int32_t e4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int t2 = 0; t2 < 4; ++t2) {
+                    const uint64_t p = v * 4 + t2;
+                    if (p >= lo && p <= hi) best = kmin(best, pack_key(e4[t2], uint32_t(p)));
+                }
+            }
+        };
+        tiny(t0, lo0, hi0);
+        tiny(t1, lo1, hi1);
+    }
     // Warp-cooperative partial-block scans.
     unsigned m0 = __ballot_sync(kFull, t0), m1 = __ballot_sync(kFull, t1);
+    if constexpr (std::is_same<E, ElemI32>::value && VPL > 0) {
+        // int32 A (BbST): ranges prefetched into L2 at once, then one range per
+        // round by the value-then-position scan (positions < 2^32: 32-bit shuffles)
+        // (whole vectors inside the array only: the last partial vector is not prefetched)
+        if (t0 && (hi0 | 3) < elem.len) prefetch_vecs_l2(elem.data, lo0 >> 2, uint32_t((hi0 >> 2) - (lo0 >> 2)) + 1u);
+        if (t1 && (hi1 | 3) < elem.len) prefetch_vecs_l2(elem.data, lo1 >> 2, uint32_t((hi1 >> 2) - (lo1 >> 2)) + 1u);
+        // ranges within 16 vectors (<= 64 cells) go two per round, one per half warp
+        unsigned s0 = __ballot_sync(kFull, t0 && (hi0 >> 2) - (lo0 >> 2) < 16);
+        unsigned s1 = __ballot_sync(kFull, t1 && (hi1 >> 2) - (lo1 >> 2) < 16);
+        m0 &= ~s0;
+        m1 &= ~s1;
+        const bool upper = lane >= 16;
+        const uint32_t j = lane & 15u;
+        while (s0 | s1) {
+            int sa = -1, sb = -1;
+            uint32_t la = 0, ha = 0, lb = 0, hb = 0;
+            auto take = [&](int& sl, uint32_t& lo, uint32_t& hi) {
+                if (s0) {
+                    sl = __ffs(s0) - 1;
+                    s0 &= s0 - 1;
+                    lo = __shfl_sync(kFull, uint32_t(lo0), sl);
+                    hi = __shfl_sync(kFull, uint32_t(hi0), sl);
+                } else if (s1) {
+                    sl = __ffs(s1) - 1;
+                    s1 &= s1 - 1;
+                    lo = __shfl_sync(kFull, uint32_t(lo1), sl);
+                    hi = __shfl_sync(kFull, uint32_t(hi1), sl);
+                }
+            };
+            take(sa, la, ha);
+            take(sb, lb, hb);
+            const uint32_t lo = upper ? lb : la, hi = upper ? hb : ha;
+            const bool live = upper ? sb >= 0 : true;
+            const uint32_t nv = (hi >> 2) - (lo >> 2) + 1u;
+            const bool in = live && j < nv;
+            const int4 x = in ? elem.load_vec((lo >> 2) + j) : make_int4(0, 0, 0, 0);
+            const uint32_t a = j == 0u ? (lo & 3u) : 0u, b = j == nv - 1u ? (hi & 3u) : 3u;
+            const int32_t mv = in ? vec_min_masked(x, a, b) : 0x7FFFFFFF;
+            const int32_t wa = __reduce_min_sync(kFull, upper ? 0x7FFFFFFF : mv);
+            const int32_t wb = __reduce_min_sync(kFull, upper ? mv : 0x7FFFFFFF);
+            const int32_t wv = upper ? wb : wa;
+            const uint32_t cand = (in && mv == wv) ? 4u * j + vec_first_eq(x, a, b, wv) : 0xFFFFFFFFu;
+            const uint32_t oa = __reduce_min_sync(kFull, upper ? 0xFFFFFFFFu : cand);
+            const uint32_t ob = __reduce_min_sync(kFull, upper ? cand : 0xFFFFFFFFu);
+            if (int(lane) == sa) best = kmin(best, pack_key(wa, (la & ~3u) + oa));
+            if (sb >= 0 && int(lane) == sb) best = kmin(best, pack_key(wb, (lb & ~3u) + ob));
+        }
+        while (m0 | m1) {
+            int sl;
+            uint32_t lo, hi;
+            if (m0) {
+                sl = __ffs(m0) - 1;
+                m0 &= m0 - 1;
+                lo = __shfl_sync(kFull, uint32_t(lo0), sl);
+                hi = __shfl_sync(kFull, uint32_t(hi0), sl);
+            } else {
+                sl = __ffs(m1) - 1;
+                m1 &= m1 - 1;
+                lo = __shfl_sync(kFull, uint32_t(lo1), sl);
+                hi = __shfl_sync(kFull, uint32_t(hi1), sl);
+            }
+            const uint64_t kb = scan_i32<VPL>(elem, lo, hi);
+            if (int(lane) == sl) best = kmin(best, kb);
+        }
+        m0 = m1 = 0;
+    }
     while (m0 | m1) {
         uint64_t tlo[TPR > 0 ? TPR : 1], thi[TPR > 0 ? TPR : 1];
         int src[TPR > 0 ? TPR : 1];
@@ -306,13 +459,13 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
         }
     }
     if (active) __stcs(reinterpret_cast<unsigned long long*>(answers + i), (unsigned long long)(done ? direct : uint64_t(key_pos(best))));
-    publish_control(pub);
 }
 
 template <class E, class QP, int VPL, int TPR, bool WPQ = false, int NT = kThreads>
 __global__ void __launch_bounds__(NT) k_query(E elem, QP qp, uint32_t k_rt, const uint64_t* __restrict__ ST,
                                               uint64_t stride, uint64_t q, uint64_t* __restrict__ answers,
                                               const CtlPublish pub) {
+    brmq::pdl_wait();
     query_body<E, QP, VPL, TPR, WPQ, NT>(elem, qp, k_rt, ST, stride, q, answers, pub);
 }
 // the k = 512 batch instance with its register budget (BRMQ_QUERY_WARPS)
@@ -322,6 +475,7 @@ __global__ void __launch_bounds__(128, BRMQ_QUERY_WARPS / 4) k_query_budget(E el
                                                                             uint64_t stride, uint64_t q,
                                                                             uint64_t* __restrict__ answers,
                                                                             const CtlPublish pub) {
+    brmq::pdl_wait();
     query_body<E, QP, VPL, TPR, false, 128>(elem, qp, k_rt, ST, stride, q, answers, pub);
 }
 
@@ -332,17 +486,17 @@ void launch_q(E e, QP qp, uint32_t k, const uint64_t* ST, uint64_t stride, uint6
               uint64_t* ans, cudaStream_t s, const CtlPublish& pub) {
     if (q <= kWarpPerQueryMax) {
         const unsigned grid = unsigned((q * 32 + kThreads - 1) / kThreads);
-        k_query<E, QP, VPL, TPR, true><<<grid, kThreads, 0, s>>>(e, qp, k, ST, stride, q, ans, pub);
+        brmq::launch_k(k_query<E, QP, VPL, TPR, true>, dim3(grid), dim3(kThreads), 0, s, e, qp, k, ST, stride, q, ans, pub);
         return;
     }
     // 128-thread CTAs: a CTA holds its SM slot until its slowest warp is done
     // (c3 h = 1: 256 -> 128 threads 1.15 -> 1.04 ms; 64 is slower on c5)
     if constexpr (VPL == 4 && TPR == 1) {
-        k_query_budget<E, QP, VPL, TPR><<<unsigned((q + 127) / 128), 128, 0, s>>>(e, qp, k, ST, stride, q,
+        brmq::launch_k(k_query_budget<E, QP, VPL, TPR>, dim3(unsigned((q + 127) / 128)), dim3(128), 0, s, e, qp, k, ST, stride, q,
                                                                                  ans, pub);
         return;
     }
-    k_query<E, QP, VPL, TPR, false, 128><<<unsigned((q + 127) / 128), 128, 0, s>>>(e, qp, k, ST, stride,
+    brmq::launch_k(k_query<E, QP, VPL, TPR, false, 128>, dim3(unsigned((q + 127) / 128)), dim3(128), 0, s, e, qp, k, ST, stride,
                                                                                   q, ans, pub);
 }
 
@@ -354,10 +508,10 @@ void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t str
     // one pending range per round: fewer registers -> more resident warps, which
     // beats batching ranges per round on this latency-bound kernel (measured)
     if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
-    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 2>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s, pub);
-    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 4>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 128) return launch_q<ElemI32, QP, 1, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     return launch_q<ElemI32, QP, 0, 0>(e, qp, k, ST, stride, q, ans, s, pub);
 }
 
@@ -399,9 +553,9 @@ __global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ 
                                                     const ulonglong2* __restrict__ Q, uint64_t q,
                                                     uint64_t* __restrict__ answers,
                                                     uint32_t* __restrict__ err, const CtlPublish pub) {
+    brmq::pdl_wait();
     const uint64_t i = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     if (i < q) naive_one(A, n, Q, i, answers, err);
-    publish_control(pub);
 }
 
 }  // namespace
@@ -409,7 +563,7 @@ __global__ void __launch_bounds__(kThreads) k_naive(const int32_t* __restrict__ 
 int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
                  uint32_t* err, cudaStream_t stream, const CtlPublish& pub) {
     if (q == 0) return 0;
-    k_naive<<<unsigned((q * 32 + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+    brmq::launch_k(k_naive, dim3(unsigned((q * 32 + kThreads - 1) / kThreads)), dim3(kThreads), 0, stream, 
         A, n, reinterpret_cast<const ulonglong2*>(Q), q, answers, err, pub);
     return 1;
 }
@@ -569,9 +723,9 @@ __global__ void __launch_bounds__(kThreads) k_query_ml(const int32_t* __restrict
                                                        uint64_t* __restrict__ answers,
                                                        uint32_t* __restrict__ err,
                                                        const CtlPublish pub) {
+    brmq::pdl_wait();
     const uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (i < q) ml_one<VEC>(A, n, k, ST, stride, sub, Q, i, answers, err);
-    publish_control(pub);
 }
 
 // ---- flat variant: power-of-two k <= 512 (<= 16 sub-blocks per block) --------
@@ -800,17 +954,17 @@ __device__ __forceinline__ void ml_flat_group(const E& elem, const QP& qp, uint3
 }
 
 template <class E, class QP, int NT>
-__global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 2048 / NT)) k_query_flat(const E elem, const QP qp, uint32_t kshift,
+__global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 32)) k_query_flat(const E elem, const QP qp, uint32_t kshift,
                                                    const uint64_t* __restrict__ ST, uint64_t stride,
                                                    const uint64_t* __restrict__ sub, uint64_t q,
                                                    uint64_t* __restrict__ answers,
                                                    const CtlPublish pub) {
+    brmq::pdl_wait();
     constexpr int kRowCap = 64;  // <= 2 rows per lane
     __shared__ uint4 s_rows[NT / 32][kRowCap];
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t g = uint64_t(blockIdx.x) * (NT / 32) + warp;
     if (g < (q + 31) / 32) ml_flat_group(elem, qp, kshift, ST, stride, sub, q, answers, g, s_rows[warp]);
-    publish_control(pub);
 }
 
 // 128-thread CTAs for large batches: a CTA holds its slot until its slowest
@@ -824,12 +978,12 @@ void launch_flat(const E& e, const QP& qp, uint32_t k, const uint64_t* ST, uint6
     // a batch whose warps all fit one wave of 1-warp CTAs (148 SMs x 32 CTAs) runs
     // with single-warp CTAs: no warp waits for a slower sibling (c2: -2.5 us)
     if (q <= uint64_t(148) * 32 * 32) {
-        k_query_flat<E, QP, 32><<<unsigned((q + 31) / 32), 32, 0, s>>>(e, qp, floor_log2_u64(k), ST,
+        brmq::launch_k(k_query_flat<E, QP, 32>, dim3(unsigned((q + 31) / 32)), dim3(32), 0, s, e, qp, floor_log2_u64(k), ST,
                                                                        stride, sub, q, answers, pub);
         return;
     }
     const unsigned g = unsigned((q + kFlatThreads - 1) / kFlatThreads);
-    k_query_flat<E, QP, kFlatThreads><<<g, kFlatThreads, 0, s>>>(e, qp, floor_log2_u64(k), ST, stride,
+    brmq::launch_k(k_query_flat<E, QP, kFlatThreads>, dim3(g), dim3(kFlatThreads), 0, s, e, qp, floor_log2_u64(k), ST, stride,
                                                                   sub, q, answers, pub);
 }
 
@@ -848,9 +1002,9 @@ int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST
         return 1;
     }
     if ((reinterpret_cast<uintptr_t>(A) & 15u) == 0)
-        k_query_ml<true><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
+        brmq::launch_k(k_query_ml<true>, dim3(grid), dim3(kThreads), 0, stream, A, n, k, ST, b, sub, Q, q, answers, err, pub);
     else
-        k_query_ml<false><<<grid, kThreads, 0, stream>>>(A, n, k, ST, b, sub, Q, q, answers, err, pub);
+        brmq::launch_k(k_query_ml<false>, dim3(grid), dim3(kThreads), 0, stream, A, n, k, ST, b, sub, Q, q, answers, err, pub);
     return 1;
 }
 

@@ -152,6 +152,7 @@ __device__ __forceinline__ uint64_t answer_chain(const ChainArgs& c, uint64_t l,
 
 __global__ void __launch_bounds__(kThreads) k_query_chain(const __grid_constant__ ChainArgs c,
                                                           const CtlPublish pub) {
+    brmq::pdl_wait();
     const uint64_t qi = uint64_t(blockIdx.x) * kThreads + threadIdx.x;
     if (qi < c.q) {
         const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(c.Q) + qi);  // streamed
@@ -168,7 +169,6 @@ __global__ void __launch_bounds__(kThreads) k_query_chain(const __grid_constant_
         }
         __stcs(reinterpret_cast<unsigned long long*>(c.ans + qi), (unsigned long long)out);
     }
-    publish_control(pub);
 }
 
 }  // namespace
@@ -194,7 +194,7 @@ int launch_query_chain(const int32_t* A, uint64_t n, const uint32_t* ks, uint32_
     a.q = q;
     a.ans = answers;
     a.err = err;
-    k_query_chain<<<unsigned((q + kThreads - 1) / kThreads), kThreads, 0, stream>>>(a, pub);
+    brmq::launch_k(k_query_chain, dim3(unsigned((q + kThreads - 1) / kThreads)), dim3(kThreads), 0, stream, a, pub);
     return 1;
 }
 

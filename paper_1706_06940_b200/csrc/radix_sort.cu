@@ -1,21 +1,32 @@
 // radix_sort.cu -- on-device LSD radix sort of (pos, origin) endpoint pairs.
 //
-// Replaces radix_sort_by_pos (contraction.cpp:27-63): LSD by 8-bit digits of
-// the 32-bit position, one up-front histogram for every digit (:35-41),
-// stable scatter per pass (:58).  Stability makes the output order identical
-// to the reference's for equal positions (collect order).
+// Replaces radix_sort_by_pos (contraction.cpp:27-63): LSD over the bits of the
+// 32-bit position, one up-front histogram for every digit (:35-41), a stable
+// scatter per pass (:58).  Stability makes the output order identical to the
+// reference's for equal positions (collect order).  The reference walks 8-bit
+// digits and skips constant bytes; here the digits are as wide as 10 bits so
+// that positions of up to 30 bits (n <= 2^30) take three passes, not four:
+//   passes P = ceil(bits / 10), widths bits / P (+1 for the first bits % P),
+//   e.g. 27 bits (n = 1e8) -> 9 + 9 + 9, 30 bits (n = 2^30) -> 10 + 10 + 10.
 //
 // B200 design (single-pass "onesweep" scheme):
 //   k_rs_hist : one read of the keys builds the histograms of all passes.
-//   k_rs_pass : per pass ONE kernel.  A CTA takes a 4096-key tile (atomic
-//               ticket => tiles start in order), ranks keys stably inside the
-//               warp with __match_any_sync, turns per-warp digit counts into
-//               tile offsets, publishes its 256 digit counts, looks back over
-//               the predecessors' epoch-tagged counts (decoupled look-back,
-//               one thread per digit) and scatters.  No separate scan kernel,
+//   k_rs_pass : per pass ONE kernel.  A CTA takes a tile (atomic ticket =>
+//               tiles start in order) of NT x ITEMS keys, item-major and
+//               lane-minor per warp (coalesced loads), and ranks them stably
+//               inside the warp: the peers of a key are found with one ballot
+//               per digit bit (a "multisplit"; __match_any_sync took 47% of
+//               the old kernel's stall samples, profiles/r02_rs_pass_*), the
+//               running per-digit count lives in a 16-bit warp-private
+//               counter.  Per digit: warp offsets, the tile's count published
+//               as a descriptor, decoupled look-back over the
+//               predecessors (one memset per sort zeroes the descriptors),
+//               and the tile is staged in shared memory sorted
+//               by digit, then written out in runs (consecutive threads ->
+//               consecutive addresses of a bucket).  No separate scan kernel,
 //               no global barrier, no status clearing between launches.
-// Only ceil(bits/8) passes run, with bits = bit_width(n-1) chosen by the
-// caller (positions < n), e.g. 27 bits -> 4 passes, the last one 3 bits wide.
+#include <cstdint>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "scan.cuh"
@@ -23,196 +34,385 @@
 namespace brmq {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kItemsLarge = 16;  // 4096-key tiles for large batches
-constexpr int kItemsSmall = 8;   // 2048-key tiles: shorter per-tile latency for small batches (measured vs 1024, 4096)
-constexpr uint64_t kSmallM = 1u << 18;
-inline int items_for(uint64_t m) { return m <= kSmallM ? kItemsSmall : kItemsLarge; }
-constexpr int kRadix = 256;
+constexpr int kMaxBits = 10;
+constexpr int kMaxRadix = 1 << kMaxBits;
 constexpr int kMaxPasses = 4;
+constexpr uint64_t kSmallM = 1u << 18;
+// (NT, ITEMS): 512 x 16 = 8192-key tiles for large batches, 256 x 8 = 2048 for
+// small ones (more tiles in flight; shorter per-tile latency)
+constexpr int kNtLarge = 512, kItemsLarge = 16;
+constexpr int kNtSmall = 256, kItemsSmall = 8;
+inline uint64_t tile_for(uint64_t m) {
+    return m <= kSmallM ? uint64_t(kNtSmall) * kItemsSmall : uint64_t(kNtLarge) * kItemsLarge;
+}
 
-__global__ void __launch_bounds__(kThreads) k_rs_hist(const uint32_t* __restrict__ keys, uint64_t m,
-                                                      int passes,
-                                                      unsigned long long* __restrict__ ghist) {
-    __shared__ uint32_t h[kMaxPasses][kRadix];
-    for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kThreads) (&h[0][0])[i] = 0;
+// Digit widths of pass p for `bits` key bits.
+struct Plan {
+    int passes;
+    int width[kMaxPasses];
+    int shift[kMaxPasses];
+};
+inline Plan plan_for(int bits) {
+    Plan pl{};
+    if (bits <= 0) return pl;
+    pl.passes = (bits + kMaxBits - 1) / kMaxBits;
+    if (pl.passes > kMaxPasses) pl.passes = kMaxPasses;
+    const int base = bits / pl.passes, extra = bits % pl.passes;
+    int sh = 0;
+    for (int p = 0; p < pl.passes; ++p) {
+        pl.width[p] = base + (p < extra ? 1 : 0);
+        pl.shift[p] = sh;
+        sh += pl.width[p];
+    }
+    return pl;
+}
+
+struct HistArgs {
+    int passes;
+    int width[kMaxPasses];
+    int shift[kMaxPasses];
+};
+
+__global__ void __launch_bounds__(256) k_rs_hist(const uint32_t* __restrict__ keys, uint64_t m,
+                                                 const __grid_constant__ HistArgs a,
+                                                 unsigned long long* __restrict__ ghist) {
+    brmq::pdl_wait();
+    __shared__ uint32_t h[kMaxPasses][kMaxRadix];
+    for (int i = threadIdx.x; i < kMaxPasses * kMaxRadix; i += 256) (&h[0][0])[i] = 0;
     __syncthreads();
-    const uint64_t stride = uint64_t(gridDim.x) * kThreads;
-    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < m; i += stride) {
+    const uint64_t stride = uint64_t(gridDim.x) * 256;
+    for (uint64_t i = uint64_t(blockIdx.x) * 256 + threadIdx.x; i < m; i += stride) {
         const uint32_t k = __ldg(keys + i);
-        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
+        for (int p = 0; p < a.passes; ++p)
+            atomicAdd(&h[p][(k >> a.shift[p]) & ((1u << a.width[p]) - 1u)], 1u);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) {
-        const uint32_t c = (&h[0][0])[i];
-        if (c) atomicAdd(ghist + i, (unsigned long long)c);
+    for (int p = 0; p < a.passes; ++p)
+        for (int d = threadIdx.x; d < (1 << a.width[p]); d += 256) {
+            const uint32_t c = h[p][d];
+            if (c) atomicAdd(ghist + p * kMaxRadix + d, (unsigned long long)c);
+        }
+}
+
+// Dynamic shared memory of k_rs_pass<NT, ITEMS>.
+template <int NT, int ITEMS>
+struct PassSmem {
+    static constexpr int NW = NT / 32;
+    static constexpr int TILE = NT * ITEMS;
+    static_assert(NW * kMaxRadix >= TILE, "the destination map reuses the warp counters");
+    // per warp: running count, then the warp's offset in the digit; afterwards
+    // reused as dest[] (the sorted slot of every tile item, in input order)
+    uint16_t whist[NW][kMaxRadix];
+    uint32_t thist[kMaxRadix];  // tile histogram (unordered smem atomics, published early)
+    uint32_t texcl[kMaxRadix];  // tile-local start of each digit
+    uint32_t gbase[kMaxRadix];  // global start of each digit's run of this tile
+    uint32_t scan[NW + 1];
+    uint32_t tile;
+    uint32_t skey[TILE], sval[TILE];  // the tile, sorted by digit (stable)
+};
+
+// Look-back descriptors: one word per (tile, digit), zeroed by the sort's memset
+// (no epochs): [top 2 bits] state 0 not ready / 1 aggregate / 2 inclusive,
+// [rest] the count.  32-bit words while m < 2^30 (half the traffic of 64-bit
+// epoch-tagged words; a tile's 1024 descriptors are the look-back's bytes).
+template <class W>
+struct Desc {
+    static constexpr int kShift = int(sizeof(W) * 8) - 2;
+    static constexpr W kMask = (W(1) << kShift) - 1;
+    static __device__ __forceinline__ W pack(uint32_t state, uint64_t v) { return (W(state) << kShift) | W(v); }
+    static __device__ __forceinline__ uint32_t state(W w) { return uint32_t(w >> kShift); }
+    static __device__ __forceinline__ uint64_t value(W w) { return uint64_t(w & kMask); }
+};
+__device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_vol(const uint64_t* p) { return ld_relaxed_u64(p); }
+__device__ __forceinline__ void st_vol(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_vol(uint64_t* p, uint64_t v) { st_relaxed_u64(p, v); }
+
+// WB: the digit width at compile time (8, 9, 10: the ballot loop unrolls), or 0
+// for a run-time width.
+template <int NT, int ITEMS, int WB, class W>
+__global__ void __launch_bounds__(NT, (NT == 512 ? 2 : 4)) k_rs_pass(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t m, int shift, int width_rt,
+    const unsigned long long* __restrict__ ghist, W* __restrict__ status,
+    uint32_t* __restrict__ ticket) {
+    brmq::pdl_wait();
+    using S = PassSmem<NT, ITEMS>;
+    using D = Desc<W>;
+    constexpr int NW = S::NW, TILE = S::TILE;
+    constexpr int DPT = kMaxRadix / NT;  // digits per thread (2 or 4), consecutive
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& sm = *reinterpret_cast<S*>(smem_raw);
+    const int width = WB > 0 ? WB : width_rt;
+    const uint32_t radix = 1u << width, dmask = radix - 1u;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+    if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < NW * kMaxRadix / 2; i += NT)
+        reinterpret_cast<uint32_t*>(&sm.whist[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kMaxRadix; i += NT) sm.thist[i] = 0u;
+    __syncthreads();
+    const uint64_t tile = sm.tile;
+    const uint64_t tbase = tile * TILE;
+    const uint64_t base = tbase + uint64_t(warp) * (32 * ITEMS);
+
+    // values are not held across the ranking: they are copied into their sorted
+    // slots afterwards by a coalesced pass (dest[] map), which keeps the kernel at
+    // 64 registers without spills
+    uint32_t key[ITEMS];
+    uint32_t rank2[(ITEMS + 1) / 2];  // two 16-bit in-warp ranks (later: sorted slots) per register
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint64_t idx = base + uint64_t(i) * 32 + lane;
+        key[i] = idx < m ? __ldcs(kin + idx) : 0u;
+    }
+
+    // 1) tile histogram (unordered), published at once: a successor's look-back
+    //    never waits on this tile's ranking
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+        if (base + uint64_t(i) * 32 + lane < m) atomicAdd(&sm.thist[(key[i] >> shift) & dmask], 1u);
+    __syncthreads();
+    uint32_t tsum = 0;
+    W* st = status + tile * kMaxRadix;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x * DPT + j;
+        const uint32_t tc = d < radix ? sm.thist[d] : 0u;
+        tsum += tc;
+        if (d < radix) st_vol(st + d, D::pack(tile == 0 ? 2u : 1u, tc));
+    }
+
+    // 2) tile-local digit starts and the global histogram's exclusive prefix
+    //    (gbase[d] gets the tile's look-back count added once it is known)
+    {
+        uint32_t ttot_unused, gtot;
+        uint32_t run = block_excl_sum<NT>(tsum, sm.scan, ttot_unused);
+        uint32_t gsum = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+            const uint32_t d = threadIdx.x * DPT + j;
+            gsum += d < radix ? uint32_t(ghist[d]) : 0u;
+        }
+        uint32_t grun = block_excl_sum<NT>(gsum, sm.scan, gtot);
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+            const uint32_t d = threadIdx.x * DPT + j;
+            if (d < radix) {
+                sm.texcl[d] = run;
+                sm.gbase[d] = grun;
+                run += sm.thist[d];
+                grun += uint32_t(ghist[d]);
+            }
+        }
+    }
+
+    // 3) stable warp ranking, item-major / lane-minor == input order.  The peers
+    //    of a key (same digit) come from one ballot per digit bit.
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = base + uint64_t(i) * 32 + lane < m;
+        const uint32_t d = (key[i] >> shift) & dmask;
+        unsigned peers = __ballot_sync(kFull, ok);
+#pragma unroll
+        for (int b = 0; b < (WB > 0 ? WB : kMaxBits); ++b) {
+            if (WB == 0 && b >= width) break;
+            const bool bit = (d >> b) & 1u;
+            const unsigned bb = __ballot_sync(kFull, bit);
+            peers &= bit ? bb : ~bb;
+        }
+        const uint32_t prev = ok ? sm.whist[warp][d] : 0u;
+        __syncwarp();
+        const uint32_t rk = prev + __popc(peers & lt);
+        rank2[i / 2] = (i & 1) ? (rank2[i / 2] | (rk << 16)) : rk;
+        if (ok && lane == unsigned(__ffs(peers) - 1)) sm.whist[warp][d] = uint16_t(prev + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // 4) per digit: the warps' offsets inside the tile's run of the digit
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x * DPT + j;
+        if (d < radix) {
+            uint32_t sum = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t c = sm.whist[w][d];
+                sm.whist[w][d] = uint16_t(sum);
+                sum += c;
+            }
+        }
+    }
+    __syncthreads();
+
+    // 5) sorted slots: keys staged at once, the slot of every item recorded in
+    //    input order (dest[] over the warp counters), then the values copied
+    //    with coalesced reads
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t d = (key[i] >> shift) & dmask;
+        const uint32_t lp = sm.texcl[d] + sm.whist[warp][d] + ((rank2[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
+        rank2[i / 2] = (i & 1) ? ((rank2[i / 2] & 0xFFFFu) | (lp << 16)) : ((rank2[i / 2] & 0xFFFF0000u) | lp);
+    }
+    __syncthreads();  // every warp is done with whist: it becomes dest[]
+    uint16_t* dest = &sm.whist[0][0];
+    const bool with_vals = vin != nullptr;  // keys only: the endpoint positions alone
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t o = warp * (32 * ITEMS) + i * 32 + lane;
+        if (tbase + o < m) {
+            const uint32_t lp = (rank2[i / 2] >> (16 * (i & 1))) & 0xFFFFu;
+            sm.skey[lp] = key[i];
+            if (with_vals) dest[o] = uint16_t(lp);
+        }
+    }
+    // 6) look-back per digit, late (this tile's ranking and staging gave the
+    //    predecessors time to turn inclusive: usually tile - 1 already is),
+    //    one predecessor at a time
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x * DPT + j;
+        if (d < radix && tile > 0) {
+            uint64_t ex = 0;
+            for (int64_t p = int64_t(tile) - 1; p >= 0; --p) {
+                const W* wp = status + uint64_t(p) * kMaxRadix + d;
+                W w = ld_vol(wp);
+                while (D::state(w) == 0u) {
+                    __nanosleep(32);
+                    w = ld_vol(wp);
+                }
+                ex += D::value(w);
+                if (D::state(w) == 2u) break;
+            }
+            st_vol(st + d, D::pack(2u, ex + sm.thist[d]));
+            sm.gbase[d] += uint32_t(ex);
+        }
+    }
+    __syncthreads();
+    if (with_vals) {
+        constexpr int U = 4;
+        for (uint32_t o0 = threadIdx.x; o0 < uint32_t(TILE); o0 += U * NT) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t o = o0 + u * NT;
+                v[u] = (o < uint32_t(TILE) && tbase + o < m) ? __ldcs(vin + tbase + o) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t o = o0 + u * NT;
+                if (o < uint32_t(TILE) && tbase + o < m) sm.sval[dest[o]] = v[u];
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t ttot = uint32_t(m - tbase < uint64_t(TILE) ? m - tbase : uint64_t(TILE));
+    for (uint32_t s = threadIdx.x; s < ttot; s += NT) {
+        const uint32_t k = sm.skey[s];
+        const uint32_t d = (k >> shift) & dmask;
+        const uint32_t out = sm.gbase[d] + (s - sm.texcl[d]);
+        kout[out] = k;
+        if (with_vals) vout[out] = sm.sval[s];
     }
 }
 
-template <int kItems>
-__global__ void __launch_bounds__(kThreads) k_rs_pass(const uint32_t* __restrict__ kin,
-                                                      const uint32_t* __restrict__ vin,
-                                                      uint32_t* __restrict__ kout,
-                                                      uint32_t* __restrict__ vout, uint64_t m,
-                                                      int shift,
-                                                      const unsigned long long* __restrict__ ghist,
-                                                      uint64_t* __restrict__ status,
-                                                      uint32_t* __restrict__ ticket,
-                                                      const uint32_t* __restrict__ epoch_dev,
-                                                      uint32_t epoch_off) {
-    const uint32_t epoch = *epoch_dev + epoch_off;
-    constexpr int kTile = kThreads * kItems;
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t whist[kWarps][kRadix];
-    __shared__ uint32_t thist[kRadix];
-    __shared__ uint32_t texcl[kRadix];
-    __shared__ unsigned long long s_base[kRadix];
-    __shared__ uint32_t s_scan[kWarps + 1];
-    __shared__ uint32_t skey[kTile], sval[kTile];  // the tile, locally sorted by digit
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const uint32_t d = threadIdx.x;  // the digit this thread publishes / looks back for
-
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&whist[0][0])[i] = 0;
-    thist[d] = 0;
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const uint64_t base = tile * kTile + uint64_t(warp) * (32 * kItems);
-
-    uint32_t key[kItems], val[kItems], dig[kItems], rank[kItems];
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = base + uint64_t(i) * 32 + lane;
-        const bool ok = idx < m;
-        key[i] = ok ? __ldg(kin + idx) : 0u;
-        val[i] = ok ? __ldg(vin + idx) : 0u;
-        dig[i] = ok ? ((key[i] >> shift) & 0xFFu) : 0x100u;  // 0x100 = no key
+template <int NT, int ITEMS, int WB, class W>
+void launch_pass(uint64_t tiles, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                 uint64_t m, int shift, int width, const unsigned long long* gh, W* status,
+                 uint32_t* ticket, cudaStream_t s) {
+    const size_t sm = sizeof(PassSmem<NT, ITEMS>);
+    static bool attr[64] = {};  // the attribute belongs to the function in each device's context
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+        cudaFuncSetAttribute(k_rs_pass<NT, ITEMS, WB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        attr[dev & 63] = true;
     }
-    // 1) tile digit histogram, published at once so successors never wait on
-    //    this tile's ranking work (decoupled look-back)
-#pragma unroll
-    for (int i = 0; i < kItems; ++i)
-        if (dig[i] < 0x100u) atomicAdd(&thist[dig[i]], 1u);
-    __syncthreads();
-    const uint32_t tcount = thist[d];
-    uint64_t* st = status + tile * kRadix;
-    st_relaxed_u64(st + d, status_pack(epoch, tile == 0 ? kStInclusive : kStAggregate, false, tcount));
+    brmq::launch_k(k_rs_pass<NT, ITEMS, WB, W>, dim3(unsigned(tiles)), dim3(NT), sm, s, kin, vin, kout, vout,
+                   m, shift, width, gh, status, ticket);
+}
 
-    // 2) stable warp-level ranking: item-major, lane-minor == input order
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const unsigned peers = __match_any_sync(kFull, dig[i]);
-        const uint32_t before = __popc(peers & lt);
-        uint32_t prev = 0;
-        if (dig[i] < 0x100u) prev = whist[warp][dig[i]];
-        __syncwarp();
-        rank[i] = prev + before;
-        if (dig[i] < 0x100u && lane == unsigned(__ffs(peers) - 1))
-            whist[warp][dig[i]] = prev + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-
-    // 3) per digit: warp offsets, global digit base, look-back over tiles
-    uint32_t sum = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = whist[w][d];
-        whist[w][d] = sum;
-        sum += c;
-    }
-    uint32_t gtot, ttot;
-    const uint32_t gex = block_excl_sum<kThreads>(uint32_t(ghist[d]), s_scan, gtot);
-    texcl[d] = block_excl_sum<kThreads>(tcount, s_scan, ttot);
-    // look-back for digit d, 8 predecessors per round (independent loads in flight)
-    uint64_t excl = 0;
-    if (tile > 0) {
-        int64_t p = int64_t(tile) - 1;
-        bool done = false;
-        while (!done) {
-            uint64_t w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                w[u] = p - u >= 0 ? ld_relaxed_u64(status + uint64_t(p - u) * kRadix + d) : 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (done) break;
-                if (p - u < 0) { done = true; break; }
-                while (status_state(w[u], epoch) == kStInvalid)
-                    w[u] = ld_relaxed_u64(status + uint64_t(p - u) * kRadix + d);
-                excl += status_value(w[u]);
-                if (status_state(w[u], epoch) == kStInclusive) done = true;
-            }
-            p -= 8;
-        }
-        st_relaxed_u64(st + d, status_pack(epoch, kStInclusive, false, excl + tcount));
-    }
-    s_base[d] = (unsigned long long)gex + excl;
-    __syncthreads();
-
-    // 4) stage the tile in shared memory sorted by digit (stable), then write
-    //    out so that consecutive threads hit consecutive addresses of a bucket
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        if (dig[i] < 0x100u) {
-            const uint32_t lp = texcl[dig[i]] + whist[warp][dig[i]] + rank[i];
-            skey[lp] = key[i];
-            sval[lp] = val[i];
-        }
-    }
-    __syncthreads();
-    for (uint32_t s = threadIdx.x; s < ttot; s += kThreads) {
-        const uint32_t k = skey[s];
-        const uint32_t dd = (k >> shift) & 0xFFu;
-        const uint64_t out = s_base[dd] + (s - texcl[dd]);
-        kout[out] = k;
-        vout[out] = sval[s];
+template <int NT, int ITEMS, class W>
+void launch_pass_w(uint64_t tiles, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                   uint64_t m, int shift, int width, const unsigned long long* gh, W* status,
+                   uint32_t* ticket, cudaStream_t s) {
+    switch (width) {
+        case 10: return launch_pass<NT, ITEMS, 10, W>(tiles, kin, vin, kout, vout, m, shift, width, gh, status, ticket, s);
+        case 9: return launch_pass<NT, ITEMS, 9, W>(tiles, kin, vin, kout, vout, m, shift, width, gh, status, ticket, s);
+        case 8: return launch_pass<NT, ITEMS, 8, W>(tiles, kin, vin, kout, vout, m, shift, width, gh, status, ticket, s);
+        default: return launch_pass<NT, ITEMS, 0, W>(tiles, kin, vin, kout, vout, m, shift, width, gh, status, ticket, s);
     }
 }
 
 }  // namespace
 
-// [ghist: 4*256 u64][tickets: 4 u32 padded to 256 B], zeroed by every sort
-size_t radix_sort_temp_bytes(uint64_t, int) { return size_t(kMaxPasses * kRadix * 8) + 256; }
+// [ghist: 4 x 1024 u64][tickets: 4 u32 padded to 256 B], zeroed by every sort
+size_t radix_sort_temp_bytes(uint64_t, int) { return size_t(kMaxPasses * kMaxRadix * 8) + 256; }
 
+// 64-bit words of look-back descriptors (32-bit descriptors while m < 2^30,
+// packed two per word)
 size_t radix_sort_status_words(uint64_t m, int bits) {
-    const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
-    const uint64_t tile = uint64_t(kThreads) * items_for(m);
-    return size_t(passes) * ((m + tile - 1) / tile) * kRadix;
+    const Plan pl = plan_for(bits);
+    const uint64_t tile = tile_for(m);
+    const size_t d = size_t(pl.passes) * ((m + tile - 1) / tile) * kMaxRadix;
+    return m < (uint64_t(1) << 30) ? (d + 1) / 2 : d;
 }
 
-int radix_sort_passes(int bits) { return bits <= 0 ? 0 : (bits + 7) / 8; }
+int radix_sort_passes(int bits) { return plan_for(bits).passes; }
 
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
                       uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
-                      bool* result_in_alt, const uint32_t* epoch_dev, uint32_t epoch_off) {
+                      bool* result_in_alt, const uint32_t* /*epoch_dev*/, uint32_t /*epoch_off*/) {
     *result_in_alt = false;
     if (m <= 1 || bits <= 0) return 0;
-    const int passes = (bits + 7) / 8;
-    const int items = items_for(m);
-    const uint64_t tiles = (m + uint64_t(kThreads) * items - 1) / (uint64_t(kThreads) * items);
+    const Plan pl = plan_for(bits);
+    const uint64_t tile = tile_for(m);
+    const uint64_t tiles = (m + tile - 1) / tile;
     auto* ghist = static_cast<unsigned long long*>(tmp);
-    auto* tickets = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxPasses * kRadix * 8);
+    auto* tickets = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxPasses * kMaxRadix * 8);
     cudaMemsetAsync(tmp, 0, radix_sort_temp_bytes(m, bits), stream);
+    pdl_break();  // a memset node precedes the histogram: plain launch
     int launches = 0;
     {
-        uint64_t blocks = (m + kThreads * 8 - 1) / (kThreads * 8);
-        if (blocks > 148 * 8) blocks = 148 * 8;
-        k_rs_hist<<<unsigned(blocks), kThreads, 0, stream>>>(keys, m, passes, ghist);
+        HistArgs ha{};
+        ha.passes = pl.passes;
+        for (int p = 0; p < pl.passes; ++p) {
+            ha.width[p] = pl.width[p];
+            ha.shift[p] = pl.shift[p];
+        }
+        uint64_t blocks = (m + 256 * 16 - 1) / (256 * 16);
+        if (blocks > 148 * 4) blocks = 148 * 4;
+        brmq::launch_k(k_rs_hist, dim3(unsigned(blocks)), dim3(256), 0, stream, keys, m, ha, ghist);
         ++launches;
     }
+    // the descriptors start zeroed (state "not ready"): one memset per sort
+    const bool narrow = m < (uint64_t(1) << 30);
+    cudaMemsetAsync(status, 0, radix_sort_status_words(m, bits) * 8, stream);
+    pdl_break();
     const uint32_t* kin = keys;
     const uint32_t* vin = vals;
     uint32_t* kout = alt_keys;
     uint32_t* vout = alt_vals;
-    for (int p = 0; p < passes; ++p) {
-        auto kern = items == kItemsSmall ? k_rs_pass<kItemsSmall> : k_rs_pass<kItemsLarge>;
-        kern<<<unsigned(tiles), kThreads, 0, stream>>>(kin, vin, kout, vout, m, 8 * p,
-                                                            ghist + p * kRadix,
-                                                            status + uint64_t(p) * tiles * kRadix,
-                                                            tickets + p, epoch_dev, epoch_off + uint32_t(p));
+    for (int p = 0; p < pl.passes; ++p) {
+        const uint64_t off = uint64_t(p) * tiles * kMaxRadix;
+        uint32_t* st32 = reinterpret_cast<uint32_t*>(status) + off;
+        uint64_t* st64 = status + off;
+        const unsigned long long* gh = ghist + p * kMaxRadix;
+        if (m <= kSmallM) {
+            if (narrow) launch_pass_w<kNtSmall, kItemsSmall>(tiles, kin, vin, kout, vout, m, pl.shift[p], pl.width[p], gh, st32, tickets + p, stream);
+            else launch_pass_w<kNtSmall, kItemsSmall>(tiles, kin, vin, kout, vout, m, pl.shift[p], pl.width[p], gh, st64, tickets + p, stream);
+        } else {
+            if (narrow) launch_pass_w<kNtLarge, kItemsLarge>(tiles, kin, vin, kout, vout, m, pl.shift[p], pl.width[p], gh, st32, tickets + p, stream);
+            else launch_pass_w<kNtLarge, kItemsLarge>(tiles, kin, vin, kout, vout, m, pl.shift[p], pl.width[p], gh, st64, tickets + p, stream);
+        }
         ++launches;
         const uint32_t* tk = kin;
         const uint32_t* tv = vin;
@@ -221,7 +421,7 @@ int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32
         kout = const_cast<uint32_t*>(tk);
         vout = const_cast<uint32_t*>(tv);
     }
-    *result_in_alt = (passes & 1) != 0;
+    *result_in_alt = (pl.passes & 1) != 0;
     return launches;
 }
 

@@ -26,6 +26,8 @@ template <int R, int T, int NT>
 __global__ void __launch_bounds__(NT) k_st_tile(uint64_t* __restrict__ ST, uint64_t b_max,
                                                 const uint64_t* __restrict__ b_dev, uint32_t base,
                                                 uint32_t D, uint32_t groups) {
+    brmq::pdl_wait();
+    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     extern __shared__ uint64_t smem[];
     const uint64_t b = b_dev ? *b_dev : b_max;
     const uint64_t s = 1ull << base;
@@ -79,7 +81,7 @@ int launch_tile(uint64_t* ST, uint64_t b, const uint64_t* b_dev, uint32_t base, 
     const uint64_t tiles = (tcount + T - 1) / T;
     const size_t sm = size_t(2) * (T + (1u << D) - 1) * R * sizeof(uint64_t);
     cudaFuncSetAttribute(k_st_tile<R, T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    k_st_tile<R, T, NT><<<unsigned(groups * tiles), NT, sm, stream>>>(ST, b, b_dev, base, D,
+    brmq::launch_k(k_st_tile<R, T, NT>, dim3(unsigned(groups * tiles)), dim3(NT), sm, stream, ST, b, b_dev, base, D,
                                                                       uint32_t(groups));
     return 1;
 }

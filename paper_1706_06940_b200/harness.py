@@ -86,3 +86,9 @@ def verify(A: np.ndarray, Q: np.ndarray, answers: np.ndarray, threads: int = 0) 
     _check(_lib.lib().brmq_verify_answers(_p(A), A.shape[0], _p(Q), Q.shape[0], _p(a), threads,
                                           C.byref(bad), C.byref(first)))
     return bad.value, first.value
+
+
+def emit_plot(csv_path, svg_path) -> None:
+    """SVG time-vs-q chart, one series per algorithm, from a harness CSV
+    (include/brmq_harness.h brmq_emit_plot)."""
+    _check(_lib.lib().brmq_emit_plot(str(csv_path).encode(), str(svg_path).encode()))

@@ -152,3 +152,46 @@ def test_gen_queries_spec():
     assert (Q[:, 0] <= Q[:, 1]).all() and (Q[:, 1] < n).all()
     m = float((Q[:, 1] - Q[:, 0]).mean())
     assert abs(m - n / 3) <= 0.02 * n / 3
+
+
+def test_memory_model_multilevel_counts_every_level():
+    """bbst-ml with h >= 3: the keys of every lower level are counted (the
+    chain solve allocates M_j for every j < h - 1, api.cu solve_chain)."""
+    from paper_1706_06940_b200 import harness as H
+    n = 10**8
+    b2, _ = H.account_memory("bbst-ml", n, 0, (32, 512))
+    b3, _ = H.account_memory("bbst-ml", n, 0, (8, 64, 512))
+    b1, _ = H.account_memory("bbst", n, 0, (512,))
+    assert b2 == b1 + 8 * (-(-n // 32))
+    assert b3 == b1 + 8 * (-(-n // 8)) + 8 * (-(-n // 64))
+
+
+def test_emit_plot(tmp_path):
+    """emit_plot: one series per algorithm, deterministic,
+    empty input is a no-op, mixed n is refused."""
+    from paper_1706_06940_b200 import InvalidArgument
+    from paper_1706_06940_b200 import harness as H
+    hdr = ("algo,n,q,k_chain,threads,runs,t_sort_ns,t_contract_ns,t_build_ns,t_answer_ns,"
+           "t_total_ns,extra_bytes,extra_pct,answers_checksum\n")
+    rows = []
+    for algo, k in (("bbst", "512"), ("bbst-con", "512"), ("st-rmq-con", "")):
+        for t in range(11):
+            q = int(10**4 * 2**t)
+            rows.append(f"{algo},100000000,{q},{k},1,7,0,0,0,0,{1000 * (t + 1) * (2 if k else 5)},0,0.0,1\n")
+    csv = tmp_path / "r.csv"
+    csv.write_text(hdr + "".join(rows))
+    svg1, svg2 = tmp_path / "a.svg", tmp_path / "b.svg"
+    H.emit_plot(csv, svg1)
+    H.emit_plot(csv, svg2)
+    text = svg1.read_text()
+    assert text.startswith("<svg") and text.rstrip().endswith("</svg>")
+    assert text.count('class="series"') == 3 and text.count("<circle") == 33
+    assert svg1.read_bytes() == svg2.read_bytes()
+    empty = tmp_path / "e.csv"
+    empty.write_text(hdr)
+    H.emit_plot(empty, tmp_path / "none.svg")
+    assert not (tmp_path / "none.svg").exists()
+    mixed = tmp_path / "m.csv"
+    mixed.write_text(hdr + rows[0] + rows[1].replace("100000000", "1000"))
+    with pytest.raises(InvalidArgument):
+        H.emit_plot(mixed, tmp_path / "m.svg")

@@ -1,0 +1,82 @@
+// cub_sort_bench.cu -- yardstick for the endpoint radix sort (tooling only; never
+// linked into libbrmq.so): cub::DeviceRadixSort::SortPairs on the same shape as
+// the BbST_CON radix pipeline's sort -- 2q (pos, origin) uint32 pairs, pos
+// uniform in [0, n), origin = (qi << 1) | right, sorted on bit_width(n - 1) bits.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/cub_sort_bench tools/cub_sort_bench.cu
+//   tools/cub_sort_bench [m=20000000] [n=1073741824] [reps=10]
+#include <cub/cub.cuh>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess) {                                                         \
+            std::fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e_));                \
+            std::exit(1);                                                                \
+        }                                                                                \
+    } while (0)
+
+static uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int main(int argc, char** argv) {
+    const uint64_t m = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 20000000ull;
+    const uint64_t n = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : (1ull << 30);
+    const int reps = argc > 3 ? std::atoi(argv[3]) : 10;
+    int bits = 0;
+    while ((1ull << bits) < n) ++bits;  // bit_width(n - 1)
+    std::vector<uint32_t> hk(m), hv(m);
+    for (uint64_t i = 0; i < m; ++i) {
+        hk[i] = uint32_t((unsigned __int128)mix64(i + 1) * n >> 64);
+        hv[i] = uint32_t(i);
+    }
+    uint32_t *k0, *v0, *k1, *v1, *flush;
+    CK(cudaMalloc(&k0, m * 4));
+    CK(cudaMalloc(&v0, m * 4));
+    CK(cudaMalloc(&k1, m * 4));
+    CK(cudaMalloc(&v1, m * 4));
+    CK(cudaMalloc(&flush, 256u << 20));
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, v0, v1, int64_t(m), 0, bits));
+    void* tmp;
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double best = 1e30, sum = 0;
+    for (int r = 0; r < reps + 2; ++r) {
+        CK(cudaMemcpy(k0, hk.data(), m * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(v0, hv.data(), m * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(flush, r, 256u << 20));  // L2 flush outside the window
+        cudaEventRecord(a);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, v0, v1, int64_t(m), 0, bits));
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (r >= 2) {
+            best = ms < best ? ms : best;
+            sum += ms;
+        }
+    }
+    std::vector<uint32_t> ok(m);
+    CK(cudaMemcpy(ok.data(), k1, m * 4, cudaMemcpyDeviceToHost));
+    bool sorted = true;
+    for (uint64_t i = 1; i < m; ++i) sorted &= ok[i - 1] <= ok[i];
+    const int passes = (bits + 7) / 8;  // CUB's default digit width for 32-bit keys on this part
+    std::printf("{\"tool\": \"cub::DeviceRadixSort::SortPairs\", \"m\": %llu, \"n\": %llu, \"bits\": %d, "
+                "\"ms_mean\": %.4f, \"ms_best\": %.4f, \"pairs_per_s\": %.4g, \"sorted\": %s, "
+                "\"bytes_per_8bit_pass_GBs\": %.1f}\n",
+                (unsigned long long)m, (unsigned long long)n, bits, sum / reps, best, m / (best * 1e-3),
+                sorted ? "true" : "false", 16.0 * m * passes / (best * 1e-3) / 1e9 / passes);
+    return 0;
+}
