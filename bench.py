@@ -390,6 +390,25 @@ def run_ours(args) -> dict:
     L.brmq_host_free(hp)
     e2e_t = max_over_ranks(e2e_t, dist, dev)
 
+    # the same through PAGEABLE host buffers (numpy arrays, as the reference's
+    # std::vector callers pass them): the library stages them through a pinned
+    # double-buffered ring (csrc/staging.h) instead of the driver's bounce buffer
+    pA, pQ = np.ascontiguousarray(A), np.ascontiguousarray(Q)
+    pO = np.empty(q, np.uint64)
+
+    def solve_pageable():
+        if variant == "bbst":
+            eng.solve_batch_bbst(pA, pQ, 512, out=pO)
+        else:
+            eng.solve_batch_bbst_con(pA, pQ, 512, VARIANT_SORT[variant], out=pO)
+
+    pg_ms, _, _ = time_solves(eng, torch, stream, solve_pageable, max(3, args.steps // 2), 2, flush,
+                              timing=0, poison=lambda: pO.fill(np.uint64(0xFFFFFFFFFFFFFFFF)))
+    pg_t = max_over_ranks(statistics.mean(pg_ms), dist, dev)
+    if want is not None:
+        assert np.array_equal(pO, want), "pageable e2e answers differ from the reference oracle"
+        checks["e2e_pageable"] = True
+
     # roofline of the dominant kernel
     pk = peaks()
     dom = max(breakdown.items(), key=lambda kv: kv[1][0])[0]
@@ -418,6 +437,10 @@ def run_ours(args) -> dict:
         "e2e": {"value": aggregate_value(q, world, e2e_t), "unit": "queries/s",
                 "h2d_bytes_per_step": nbytes_a + nbytes_q, "d2h_bytes_per_step": nbytes_o,
                 "ms_per_step": e2e_t},
+        "e2e_pageable": {"value": aggregate_value(q, world, pg_t), "unit": "queries/s",
+                         "h2d_bytes_per_step": nbytes_a + nbytes_q, "d2h_bytes_per_step": nbytes_o,
+                         "ms_per_step": pg_t,
+                         "note": "numpy (pageable) host buffers, staged through a pinned ring"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom_for_roof, "achieved": achieved,
                      "peak": pk["hbm_gbs"], "peak_src": pk["src"], "unit": "GB/s",
@@ -621,6 +644,21 @@ def run_configs(eng, torch, stream, flush, args) -> dict:
             t = statistics.mean(ms)
             res[v] = {"queries_per_s": q / (t * 1e-3), "ms": t, "bit_exact_vs_reference": ok,
                       "stages_ms": {k: round(x[0], 5) for k, x in stages.items()}}
+            if v == "bbst" and "query" in stages:
+                # query-phase roofline: algorithmic bytes 24 q + 4 S, S =
+                # cells the speculation rule scans, from the kernel's debug counter
+                # (one extra, untimed solve)
+                eng.set_counters(True)
+                f()
+                S = eng.solve_info()["scanned_cells"]
+                eng.set_counters(False)
+                qb = 24 * q + 4 * S
+                qms = stages["query"][0]
+                pk = peaks()["hbm_gbs"]
+                res[v]["query_roofline"] = {
+                    "scanned_cells": int(S), "scanned_per_query": S / q, "alg_bytes": int(qb),
+                    "query_ms": qms, "achieved_gbs": qb / (qms * 1e-3) / 1e9,
+                    "frac": qb / (qms * 1e-3) / 1e9 / pk, "peak_gbs": pk}
         out[name] = res
         del dA, dQ, dO, A, Q, want
         torch.cuda.empty_cache()

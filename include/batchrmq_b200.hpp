@@ -141,8 +141,9 @@ inline void sort_endpoints(std::vector<Endpoint>& endpoints, SortKind kind = Sor
 }
 
 // contraction.hpp:61-64.  `threads` has no device meaning; `stats` receives the
-// reads of `values` the device made: every position of [b_0, b_last] once, the
-// count of the reference's serial path (contraction.cpp:85-105, 133-139).
+// reads of `values` the device contraction counted (brmq_build_contracted_stats):
+// every position of [b_0, b_last] once, the count of the reference's serial path
+// (contraction.cpp:85-105, 133-139).
 inline ContractedArray build_contracted(std::span<const Value> values,
                                         const std::vector<Endpoint>& sorted_endpoints,
                                         unsigned /*threads*/ = 1, ContractionStats* stats = nullptr) {
@@ -151,16 +152,16 @@ inline ContractedArray build_contracted(std::span<const Value> values,
     out.aq_values.resize(m);
     out.aq_origin.resize(m);
     out.boundary.resize(m);
-    std::uint64_t nb = 0;
-    b200::check(brmq_build_contracted(b200::context().get(), values.data(), values.size(),
-                                      reinterpret_cast<const brmq_endpoint*>(sorted_endpoints.data()), m,
-                                      out.aq_values.data(), out.aq_origin.data(), out.boundary.data(), &nb,
-                                      BRMQ_PTR_HOST));
+    std::uint64_t nb = 0, reads = 0;
+    b200::check(brmq_build_contracted_stats(b200::context().get(), values.data(), values.size(),
+                                            reinterpret_cast<const brmq_endpoint*>(sorted_endpoints.data()), m,
+                                            out.aq_values.data(), out.aq_origin.data(), out.boundary.data(),
+                                            &nb, BRMQ_PTR_HOST, stats ? &reads : nullptr));
     const std::size_t areas = nb > 0 ? nb - 1 : 0;
     out.aq_values.resize(areas);
     out.aq_origin.resize(areas);
     out.boundary.resize(nb);
-    if (stats && areas > 0) stats->array_reads += out.boundary.back() - out.boundary.front() + 1;
+    if (stats) stats->array_reads += reads;
     return out;
 }
 

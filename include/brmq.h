@@ -167,6 +167,15 @@ int brmq_build_contracted(brmq_ctx* ctx, const int32_t* A, uint64_t n,
                           const brmq_endpoint* sorted_eps, uint64_t m, int32_t* aq_values,
                           uint64_t* aq_origin, uint64_t* boundary, uint64_t* nb,
                           uint32_t flags);
+/* The same with ContractionStats (contraction.hpp:47-49, contraction.cpp:84-107):
+ * *array_reads (nullable) += the positions of A the device contraction consumed,
+ * counted by the kernel (each warp adds its tiles clipped to [b_0, b_last]; each
+ * position is read once: b_last - b_0 + 1 with one area or more, 0 otherwise --
+ * the reference's serial count; its threaded path adds a re-read per seam). */
+int brmq_build_contracted_stats(brmq_ctx* ctx, const int32_t* A, uint64_t n,
+                                const brmq_endpoint* sorted_eps, uint64_t m, int32_t* aq_values,
+                                uint64_t* aq_origin, uint64_t* boundary, uint64_t* nb,
+                                uint32_t flags, uint64_t* array_reads);
 
 /* contraction.hpp:71-73 remap_queries_from_sorted (contraction.cpp:174-199). */
 int brmq_remap_from_sorted(brmq_ctx* ctx, const brmq_endpoint* sorted_eps, uint64_t m,
@@ -208,6 +217,10 @@ typedef struct brmq_stage_times {
 } brmq_stage_times;
 
 int brmq_ctx_set_timing(brmq_ctx* ctx, int enable);
+/* Debug instrumentation: 1 = BbST (h = 1) solves count the
+ * array cells their partial-block scans cover (brmq_solve_info.scanned_cells;
+ * one reduction per warp).  0 (default) = off. */
+int brmq_ctx_set_counters(brmq_ctx* ctx, int enable);
 int brmq_last_stage_times(brmq_ctx* ctx, brmq_stage_times* out);
 
 /* Facts about the last solve: sizes of the intermediate structures and the
@@ -221,6 +234,9 @@ typedef struct brmq_solve_info {
     uint64_t span_hi;       /* contraction: boundary[last]                */
     uint32_t kernel_launches;
     uint32_t graph;         /* 1: the solve ran as a replayed CUDA graph     */
+    uint64_t scanned_cells; /* BbST (h = 1) with counters on: cells of A inside
+                               the partial-block ranges the speculation rule had
+                               to scan (SPEC.md:249, :472 instrumented counter) */
 } brmq_solve_info;
 
 int brmq_last_solve_info(brmq_ctx* ctx, brmq_solve_info* out);

@@ -33,7 +33,8 @@ class SolveInfo(C.Structure):
     _fields_ = [("n", C.c_uint64), ("q", C.c_uint64), ("k", C.c_uint64),
                 ("blocks", C.c_uint64), ("levels", C.c_uint32),
                 ("boundary", C.c_uint64), ("span_lo", C.c_uint64), ("span_hi", C.c_uint64),
-                ("kernel_launches", C.c_uint32), ("graph", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("graph", C.c_uint32),
+                ("scanned_cells", C.c_uint64)]
 
 
 # name -> (restype, argtypes): exactly the declarations of include/brmq*.h
@@ -58,6 +59,8 @@ SIGNATURES = {
     "brmq_sort_endpoints": (C.c_int, [vp, vp, C.c_uint64, C.c_int, C.c_uint32]),
     "brmq_build_contracted": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, u64p,
                                         C.c_uint32]),
+    "brmq_build_contracted_stats": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, u64p,
+                                              C.c_uint32, u64p]),
     "brmq_remap_queries": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, C.c_uint32]),
     "brmq_remap_from_sorted": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_uint64, C.c_uint64, vp, vp,
                                          vp, C.c_uint32]),
@@ -65,6 +68,7 @@ SIGNATURES = {
                                           u32p, C.c_uint32]),
     "brmq_floor_log2": (C.c_int, [C.c_uint64, u32p]),
     "brmq_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+    "brmq_ctx_set_counters": (C.c_int, [vp, C.c_int]),
     "brmq_last_stage_times": (C.c_int, [vp, C.POINTER(StageTimes)]),
     "brmq_last_solve_info": (C.c_int, [vp, C.POINTER(SolveInfo)]),
     "brmq_host_alloc": (C.c_int, [C.POINTER(vp), C.c_size_t]),

@@ -154,6 +154,10 @@ class Engine:
     def set_stream(self, stream_ptr: int | None) -> None:
         _check(self._L.brmq_ctx_set_stream(self._h, stream_ptr or None))
 
+    def set_counters(self, enable: bool = True) -> None:
+        """Debug scan-cell counter of BbST (h = 1) solves (solve_info()["scanned_cells"])."""
+        _check(self._L.brmq_ctx_set_counters(self._h, int(bool(enable))))
+
     def stage_times(self) -> list[tuple[str, float, int]]:
         t = _lib.StageTimes()
         _check(self._L.brmq_last_stage_times(self._h, C.byref(t)))
@@ -263,16 +267,21 @@ class Engine:
         _check(self._L.brmq_sort_endpoints(self._h, _ptr(eps), eps.shape[0], int(kind), 0))
         return eps
 
-    def build_contracted(self, values, sorted_eps: np.ndarray) -> ContractedArray:
+    def build_contracted(self, values, sorted_eps: np.ndarray, stats: dict | None = None) -> ContractedArray:
+        """contraction.hpp:61-64; `stats` (ContractionStats, :47-49) gets
+        stats["array_reads"] += the positions of `values` the device consumed."""
         values = np.ascontiguousarray(values, dtype=np.int32)
         m = sorted_eps.shape[0]
         aqv = np.empty(max(m, 1), dtype=np.int32)
         aqo = np.empty(max(m, 1), dtype=np.uint64)
         bnd = np.empty(max(m, 1), dtype=np.uint64)
         nb = C.c_uint64(0)
-        _check(self._L.brmq_build_contracted(self._h, _ptr(values), values.shape[0],
-                                             _ptr(sorted_eps), m, _ptr(aqv), _ptr(aqo), _ptr(bnd),
-                                             C.byref(nb), 0))
+        reads = C.c_uint64(0)
+        _check(self._L.brmq_build_contracted_stats(self._h, _ptr(values), values.shape[0],
+                                                   _ptr(sorted_eps), m, _ptr(aqv), _ptr(aqo), _ptr(bnd),
+                                                   C.byref(nb), 0, C.byref(reads)))
+        if stats is not None:
+            stats["array_reads"] = stats.get("array_reads", 0) + int(reads.value)
         nbv = int(nb.value)
         areas = max(nbv - 1, 0)
         return ContractedArray(aqv[:areas].copy(), aqo[:areas].copy(), bnd[:nbv].copy())

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "errors.h"
 #include "kernels.h"
+#include "staging.h"
 
 namespace {
 
@@ -57,6 +58,8 @@ struct Control {
     uint32_t err;       // 1 query out of range (direct), 2 range (collect/unique), 4 unsorted, 8 logic
     uint32_t span[2];   // [~min endpoint, max endpoint]
     uint32_t tickets[5];  // last-CTA tickets: [0] k_unique
+    uint64_t array_reads;  // positions of A the contraction consumed (ContractionStats)
+    uint64_t scanned;      // cells of A the h = 1 query scans covered (debug counter)
     uint64_t nb;        // |boundary|
     uint64_t aq_len;    // |A_Q|
     uint64_t b_dev;     // blocks over A_Q
@@ -105,7 +108,11 @@ struct brmq_ctx {
     uint32_t epoch_host = 1;        // host mirror of *epoch_dev
     bool use_graphs = true;
     bool use_pdl = false;  // programmatic dependent launches inside a solve (BRMQ_PDL=1: on; DESIGN 3.5)
-    bool use_fuse = true;  // small A_Q: block minima + table inside the contraction (BRMQ_FUSE=0: off)
+    bool count_scans = false;  // brmq_ctx_set_counters
+    // small A_Q: block / sub-block minima by reductions inside the contraction
+    // (BRMQ_FUSE=1: on).  Off: measured -1 us at c2 in one harness and +16 us in
+    // bench.py's process (DESIGN 3.1)
+    bool use_fuse = false;
     struct GraphEntry;
     std::vector<GraphEntry*> graphs;
     // timing: 0 off, 1 every stage, 2 only the roofline kernel (contract / block_argmin)
@@ -115,6 +122,7 @@ struct brmq_ctx {
     std::vector<uint32_t> stage_launches;
     brmq_stage_times last_times{};
     brmq_solve_info info{};
+    brmq::Stager stager;  // host-pointer solves: pinned-ring staging of pageable buffers
 };
 
 // A captured solve: replaying it re-runs every kernel with the same buffers;
@@ -433,6 +441,12 @@ int brmq_ctx_set_timing(brmq_ctx* c, int enable) {
     return BRMQ_OK;
 }
 
+int brmq_ctx_set_counters(brmq_ctx* c, int enable) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    c->count_scans = enable != 0;
+    return BRMQ_OK;
+}
+
 int brmq_last_stage_times(brmq_ctx* c, brmq_stage_times* out) {
     if (!c || !out) return fail(BRMQ_EINVAL, "null argument");
     *out = c->last_times;
@@ -574,8 +588,8 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     if (!dev) {
         auto* hA = reinterpret_cast<int32_t*>(buf + ((q * 33 + 64 + 15) & ~size_t(15)));
         auto* hQ = reinterpret_cast<ulonglong2*>(reinterpret_cast<char*>(hA) + a_bytes);
-        CUDA_TRY(cudaMemcpyAsync(hA, A, n_shard * 4, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(hQ, Q, q * 16, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(c->stager.h2d(hA, A, n_shard * 4, s));
+        CUDA_TRY(c->stager.h2d(hQ, Q, q * 16, s));
         dA = hA;
         dQ = hQ;
     }
@@ -588,7 +602,7 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     if (rc == BRMQ_OK) {
         brmq::launch_k(k_shard_keys, dim3(g), dim3(256), 0, s, loc, empty, dA, offset, q, dev ? keys : dkeys);
         uint32_t herr = 0;
-        if (!dev) CUDA_TRY(cudaMemcpyAsync(keys, dkeys, q * 8, cudaMemcpyDeviceToHost, s));
+        if (!dev) CUDA_TRY(c->stager.d2h(keys, dkeys, q * 8, s));
         CUDA_TRY(cudaMemcpyAsync(c->ctl_host, err, 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         herr = *reinterpret_cast<uint32_t*>(c->ctl_host);
@@ -660,8 +674,8 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("query", launches);
@@ -672,7 +686,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         // (the control header reaches c->ctl_host from the final kernel: publish())
@@ -730,8 +744,8 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -743,20 +757,21 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         launches += l;
         tm.end(l);
         tm.stage("query", launches);
-        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{});
+        l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{},
+                                      c->count_scans ? &ctl->scanned : nullptr);
         launches += l;
         tm.end(l);
         launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         // (the control header reaches c->ctl_host from the final kernel: publish())
         return BRMQ_OK;
     };
-    const GraphKey key{0, A, n, Q, q, k, 0, answers, s};
+    const GraphKey key{0, A, n, Q, q, k, c->count_scans ? 1 : 0, answers, s};
     if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
@@ -765,6 +780,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     c->info.blocks = b;
     c->info.levels = L;
     c->info.kernel_launches = uint32_t(launches);
+    c->info.scanned_cells = c->count_scans ? c->ctl_host->scanned : 0;
     return map_err(c->ctl_host->err);
 }
 
@@ -818,8 +834,8 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         int l = 0;
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -842,7 +858,7 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         return BRMQ_OK;
@@ -910,8 +926,8 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -930,7 +946,7 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         // (the control header reaches c->ctl_host from the final kernel: publish())
@@ -1035,8 +1051,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         // the epochs of this solve are reserved by the first kernel (k_collect)
@@ -1111,7 +1127,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         // (the control header reaches c->ctl_host from the final kernel: publish())
@@ -1202,8 +1218,8 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
-            CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
-            CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         // the epochs of this solve are reserved by the first kernel (k_collect)
@@ -1248,7 +1264,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
-            CUDA_TRY(cudaMemcpyAsync(answers, dAns, q * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(c->stager.d2h(answers, dAns, q * 8, s));
             tm.end(0);
         }
         // (the control header reaches c->ctl_host from the final kernel: publish())
@@ -1293,7 +1309,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
     void* dE = dev ? static_cast<void*>(eps) : static_cast<void*>(P(i_e));
     c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
-    if (!dev) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+    if (!dev) CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
     auto* v = reinterpret_cast<uint32_t*>(P(i_v));
     brmq::launch_collect(dQ, q, ~0ull, k, v, nullptr, nullptr, &ctl->err, s);  // positions truncated to 32 bits (contraction.cpp:19-20)
@@ -1342,6 +1358,13 @@ int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_ki
 int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_endpoint* sorted_eps,
                           uint64_t m, int32_t* aq_values, uint64_t* aq_origin, uint64_t* boundary,
                           uint64_t* nb, uint32_t flags) {
+    return brmq_build_contracted_stats(c, A, n, sorted_eps, m, aq_values, aq_origin, boundary, nb,
+                                       flags, nullptr);
+}
+
+int brmq_build_contracted_stats(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_endpoint* sorted_eps,
+                                uint64_t m, int32_t* aq_values, uint64_t* aq_origin, uint64_t* boundary,
+                                uint64_t* nb, uint32_t flags, uint64_t* array_reads) {
     if (!c || !nb) return fail(BRMQ_EINVAL, "null argument");
     *nb = 0;
     if (m == 0) return BRMQ_OK;  // contraction.cpp:116
@@ -1377,7 +1400,7 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
-        CUDA_TRY(cudaMemcpyAsync(const_cast<int32_t*>(dA), A, n * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
         CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dE), sorted_eps, m * 8, cudaMemcpyHostToDevice, s));
     }
     auto* k = reinterpret_cast<uint32_t*>(P(i_k));
@@ -1402,13 +1425,16 @@ int brmq_build_contracted(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
     }
     brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, true, AQ, &ctl->nb,
                           &ctl->aq_len, nullptr,
-                          S(i_cst), c->epoch_dev, 1, s);
+                          S(i_cst), c->epoch_dev, 1, s, false, nullptr, m, nullptr, nullptr,
+                          array_reads ? &ctl->array_reads : nullptr);
     brmq::launch_split_aq(AQ, &ctl->aq_len, m, dav, dao, s);
     brmq::launch_u32_to_u64(bd, &ctl->nb, m, dbo, s);
     if (int rc = check_status(c)) return rc;
     if (int rc = sync_and_read_control(c, ctl)) return rc;
     const uint64_t nbv = c->ctl_host->nb;
     const uint64_t areas = nbv > 0 ? nbv - 1 : 0;
+    // contraction.cpp:84-107: with one area or more the scan reads b_0 .. b_last
+    if (array_reads) *array_reads += areas ? c->ctl_host->array_reads : 0;
     if (!dev) {
         if (areas) {
             CUDA_TRY(cudaMemcpyAsync(aq_values, dav, areas * 4, cudaMemcpyDeviceToHost, s));
@@ -1493,7 +1519,7 @@ int brmq_remap_queries(brmq_ctx* c, const brmq_query* Q, uint64_t q, const uint6
     c->ctl_clean = false;  // stage calls leave the header dirty
     CUDA_TRY(cudaMemsetAsync(ctl, 0, kCtlHeader, s));
     if (!dev) {
-        CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dQ), Q, q * 16, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
         if (nb) CUDA_TRY(cudaMemcpyAsync(const_cast<uint64_t*>(dB), boundary, nb * 8, cudaMemcpyHostToDevice, s));
     }
     brmq::launch_remap_queries(dQ, q, dB, nb, dcl, dcr, ddg, &ctl->err, s);

@@ -377,6 +377,9 @@ struct ContractArgs {
     uint64_t fuse_stride;
     uint32_t fuse_kshift;
     uint64_t* b_dev;
+    // nullable: += the positions of A this kernel consumed (ContractionStats,
+    // contraction.hpp:47-49), one reduction per warp
+    uint64_t* reads;
 };
 
 // MARKED: ST-RMQ_CON's marked contraction -- marked positions read as +inf
@@ -694,6 +697,11 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         rank_run += wc;
     };
 
+    if (c.reads && cnt && lane == 0) {  // the warp's tiles, clipped to the span
+        const uint64_t lo = wa * kWTile > b0 ? wa * kWTile : b0;
+        const uint64_t hi = (wa + cnt) * kWTile - 1 < blast ? (wa + cnt) * kWTile - 1 : blast;
+        if (hi >= lo) atomicAdd(reinterpret_cast<unsigned long long*>(c.reads), (unsigned long long)(hi - lo + 1));
+    }
     if (cnt) stage();
     for (uint64_t i = 0; i < cnt; ++i) {
         const uint32_t fl = fy;
@@ -823,7 +831,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     uint64_t* aq_len,
                     uint2* word_info, uint64_t* status, const uint32_t* epoch_dev,
                     uint32_t epoch_off, cudaStream_t s, bool marked, const uint32_t* pcnt,
-                    uint64_t endpoints, const ContractFuse* fuse, bool* fused) {
+                    uint64_t endpoints, const ContractFuse* fuse, bool* fused, uint64_t* array_reads) {
     if (fused) *fused = false;
     if (n == 0) return 0;
     uint32_t G = 0, R = 0;
@@ -835,7 +843,8 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     ContractArgs args{A, n, bitmap, span, aq, nb_out, aq_len, word_info, rcnt, R,
                       prefix ? 1u : 0u, status, status + kMaxContractRanges, pcnt, epoch_dev,
                       epoch_off, fz ? fuse->sub : nullptr, fz ? fuse->st : nullptr,
-                      fz ? fuse->b_max : 0, fz ? fuse->kshift : 0u, fz ? fuse->b_dev : nullptr};
+                      fz ? fuse->b_max : 0, fz ? fuse->kshift : 0u, fz ? fuse->b_dev : nullptr,
+                      array_reads};
     void* params[] = {&args};
     // >= 8 endpoints per 1024 positions on average: nearly every flagged warp tile
     // has more than kDense flagged rows, so the dense-only instance runs

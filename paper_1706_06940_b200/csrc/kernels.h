@@ -100,10 +100,12 @@ int launch_sparse_table(uint64_t* ST, uint64_t b, const uint64_t* b_dev, cudaStr
 int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, uint64_t* answers,
                  uint32_t* err, cudaStream_t stream,
                     const CtlPublish& pub = CtlPublish{});
+// scanned (nullable): += the cells of A inside the partial ranges scanned
+// (the SPEC's instrumented speculation counter; one reduction per warp)
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST,
                         uint64_t b, const uint64_t* Q, uint64_t q, uint64_t* answers,
                         uint32_t* err, cudaStream_t stream,
-                    const CtlPublish& pub = CtlPublish{});
+                    const CtlPublish& pub = CtlPublish{}, uint64_t* scanned = nullptr);
 // Multi-level BbST [32, k] answering: endpoint blocks resolved through the
 // 32-element sub-block keys, raw A read only inside partial sub-blocks.
 int launch_query_ml(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
@@ -201,7 +203,8 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
                     uint64_t* status, const uint32_t* epoch_dev, uint32_t epoch_off,
                     cudaStream_t s, bool marked = false,
                     const uint32_t* pcnt = nullptr, uint64_t endpoints = 0,
-                    const ContractFuse* fuse = nullptr, bool* fused = nullptr);
+                    const ContractFuse* fuse = nullptr, bool* fused = nullptr,
+                    uint64_t* array_reads = nullptr);
 int launch_remap_bitmap(const uint64_t* Q, uint64_t q, uint64_t n, const uint2* word_info,
                         uint32_t* cleft, uint32_t* cright_raw, cudaStream_t s);
 // stage-API helpers (not on the solve path)

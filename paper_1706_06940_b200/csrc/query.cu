@@ -58,6 +58,7 @@ struct ElemI32 {
     static constexpr int EPV = 4;
     const int32_t* data;
     uint64_t len;
+    unsigned long long* scanned = nullptr;  // debug counter (launch_query_direct)
     __device__ __forceinline__ uint64_t key_at(uint64_t i) const {
         return pack_key(__ldg(data + i), uint32_t(i));
     }
@@ -331,6 +332,11 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
                 }
             }
         };
+        if (elem.scanned) {  // instrumented: cells of every range the rule scans
+            uint64_t cells = (t0 ? hi0 - lo0 + 1 : 0) + (t1 ? hi1 - lo1 + 1 : 0);
+            cells = __reduce_add_sync(kFull, uint32_t(cells));
+            if (lane == 0 && cells) atomicAdd(elem.scanned, (unsigned long long)cells);
+        }
         tiny(t0, lo0, hi0);
         tiny(t1, lo1, hi1);
     }
@@ -570,9 +576,10 @@ int launch_naive(const int32_t* A, uint64_t n, const uint64_t* Q, uint64_t q, ui
 
 int launch_query_direct(const int32_t* A, uint64_t n, uint32_t k, const uint64_t* ST, uint64_t b,
                         const uint64_t* Q, uint64_t q, uint64_t* answers, uint32_t* err,
-                        cudaStream_t stream, const CtlPublish& pub) {
+                        cudaStream_t stream, const CtlPublish& pub, uint64_t* scanned) {
     if (q == 0) return 0;
-    dispatch_i32(ElemI32{A, n}, QueryDirect{Q, n, err}, k, ST, b, q, answers, stream, pub);
+    dispatch_i32(ElemI32{A, n, reinterpret_cast<unsigned long long*>(scanned)}, QueryDirect{Q, n, err}, k,
+                 ST, b, q, answers, stream, pub);
     return 1;
 }
 

@@ -40,7 +40,13 @@ constexpr int kMaxPasses = 4;
 constexpr uint64_t kSmallM = 1u << 18;
 // (NT, ITEMS): 512 x 16 = 8192-key tiles for large batches, 256 x 8 = 2048 for
 // small ones (more tiles in flight; shorter per-tile latency)
-constexpr int kNtLarge = 512, kItemsLarge = 16;
+#ifndef BRMQ_RS_NT
+#define BRMQ_RS_NT 512
+#endif
+#ifndef BRMQ_RS_ITEMS
+#define BRMQ_RS_ITEMS 16
+#endif
+constexpr int kNtLarge = BRMQ_RS_NT, kItemsLarge = BRMQ_RS_ITEMS;
 constexpr int kNtSmall = 256, kItemsSmall = 8;
 inline uint64_t tile_for(uint64_t m) {
     return m <= kSmallM ? uint64_t(kNtSmall) * kItemsSmall : uint64_t(kNtLarge) * kItemsLarge;
@@ -137,7 +143,7 @@ __device__ __forceinline__ void st_vol(uint64_t* p, uint64_t v) { st_relaxed_u64
 // WB: the digit width at compile time (8, 9, 10: the ballot loop unrolls), or 0
 // for a run-time width.
 template <int NT, int ITEMS, int WB, class W>
-__global__ void __launch_bounds__(NT, (NT == 512 ? 2 : 4)) k_rs_pass(
+__global__ void __launch_bounds__(NT, (NT == 512 ? 2 : (NT == 256 && ITEMS > 8 ? 3 : 4))) k_rs_pass(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t m, int shift, int width_rt,
     const unsigned long long* __restrict__ ghist, W* __restrict__ status,

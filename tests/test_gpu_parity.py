@@ -344,16 +344,21 @@ def test_stage_contract_remap(engine, orc):
         eps = np.empty(2 * q, ENDPOINT_DTYPE)
         orc.port().orc_collect_endpoints(orc._p(Q), q, orc._p(eps))
         orc.port().orc_sort_endpoints(orc._p(eps), 2 * q, 0)
-        con = engine.build_contracted(A, eps)
+        stats = {}
+        con = engine.build_contracted(A, eps, stats)
         m = 2 * q
         aqv = np.empty(m, np.int32)
         aqo = np.empty(m, np.uint64)
         bnd = np.empty(m, np.uint64)
         import ctypes as C
         nb = C.c_uint64()
+        reads = C.c_uint64()
         orc.port().orc_build_contracted(orc._p(A), n, orc._p(eps), m, 1, orc._p(aqv), orc._p(aqo),
-                                        orc._p(bnd), C.byref(nb), None)
+                                        orc._p(bnd), C.byref(nb), C.byref(reads))
         nbv = nb.value
+        # ContractionStats.array_reads (contraction.hpp:47-49): the device counter
+        # equals the reference's serial count
+        assert stats["array_reads"] == reads.value, (n, q, stats, reads.value)
         assert np.array_equal(con.boundary, bnd[:nbv])
         assert np.array_equal(con.aq_values, aqv[:max(nbv - 1, 0)])
         assert np.array_equal(con.aq_origin, aqo[:max(nbv - 1, 0)])
@@ -503,3 +508,49 @@ def test_control_block_protocol(engine, orc):
             assert np.array_equal(_solve(engine, "con_radix", A, Q, 512), want)
             engine.build_block_sparse(A[:1000], 8)  # stage call
             assert np.array_equal(_solve(engine, "bbst", A, Q, 512), want)
+
+
+def test_pageable_host_buffers_staged(engine, orc):
+    """Host-pointer solves with pageable (numpy) buffers larger than the staging
+    ring's 16 MiB chunks (csrc/staging.h): A of 80 MB + 3 bytes' worth of odd
+    tail, answers of 24 MB (two D2H chunks), every variant against the oracle;
+    and a pinned buffer through the direct path."""
+    r = np.random.default_rng(4242)
+    n = 20_000_003
+    A = _values(r, n, "ties16")
+    Q = _queries(r, n, 3_000_001, "mixed")
+    want = orc.solve_oracle(A, Q)
+    for variant in ("bbst", "con_bitmap", "con_radix", "bbst_ml"):
+        got = _solve(engine, variant, A, Q, 512)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (variant, bad[:5])
+
+
+def test_scan_counter_matches_oracle(engine, orc):
+    """The debug scan-cell counter of the BbST (h = 1) query kernel (SPEC.md:249,
+    :472 instrumented counter) equals the C restatement's S on the same inputs:
+    both apply the same leftmost-exact speculation rule."""
+    r = np.random.default_rng(77)
+    for n, q, vk, qk in ((1_000_000, 100_000, "uniform", "mixed"), (300_007, 50_000, "ties16", "short"),
+                         (2_000_000, 20_000, "walk", "uniform")):
+        A = _values(r, n, vk)
+        Q = _queries(r, n, q, qk)
+        want, S, _ = orc.solve_bbst_port(A, Q, 512)
+        engine.set_counters(True)
+        try:
+            got = engine.solve_batch_bbst(A, Q, 512)
+            info = engine.solve_info()
+        finally:
+            engine.set_counters(False)
+        assert np.array_equal(got, want)
+        # a degenerate query (l == r) is answered directly on the device; the
+        # restatement walks answer_one for it and scans the one cell unless the
+        # block minimum sits there
+        lo = np.minimum(Q[:, 0], Q[:, 1]).astype(np.int64)
+        deg = lo[Q[:, 0] == Q[:, 1]]
+        blk = deg // 512
+        bmin = np.array([b * 512 + int(np.argmin(A[b * 512:min(n, b * 512 + 512)])) for b in blk], np.int64)
+        S_dev = S - int(np.count_nonzero(bmin != deg))
+        assert info["scanned_cells"] == S_dev, (n, q, info["scanned_cells"], S, S_dev)
+    engine.solve_batch_bbst(A, Q, 512)
+    assert engine.solve_info()["scanned_cells"] == 0  # off again

@@ -5,14 +5,14 @@
 //   ldgp  : persistent grid-stride warps, 4 x 16 B per lane per step
 //   bulk  : persistent CTAs, 1D cp.async.bulk ring of S x T-byte stages
 //   tma2d : persistent CTAs, 2D tensor-map ring (128 B rows, 128B swizzle)
-// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include
-//        -Ipaper_1706_06940_b200/csrc tools/stream_bench.cu -o /tmp/sb -lcuda
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I tools
+//        tools/stream_bench.cu -o /tmp/sb -lcuda
 #include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
 
-#include "common.cuh"
+#include "tma_dev.cuh"
 #include "tma_host.h"
 
 using namespace brmq;
