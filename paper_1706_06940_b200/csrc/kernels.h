@@ -90,7 +90,6 @@ int launch_block_argmin_keys_ml(const uint64_t* K, uint64_t len_max, const uint6
                                 cudaStream_t stream);
 int launch_block_argmin_ml(const int32_t* A, uint64_t n, uint32_t k, uint64_t* keys,
                            uint64_t* sub, cudaStream_t stream);
-
 // ---------------------------------------------------------------- sparse_table.cu
 // Levels 1..L-1 of the block Sparse Table, row e at ST + e*b (row 0 = level 0).
 // b_dev (nullable) holds the true block count <= b (rows stay strided by b).

@@ -36,11 +36,11 @@ namespace brmq {
 namespace {
 
 constexpr int kThreads = 256;
-// k_query's register budget for the k = 512 batch instance (4 vectors per lane): 40
-// resident warps per SM (<= 48 registers; the other instances would spill).  The
-// unconstrained build took 64 registers (32 warps); c3 / c4 / c5 query phases
-// 0.906 / 0.271 / 0.268 -> 0.875 / 0.261 / 0.247 ms (48 warps at 40 registers
-// spilled and lost: 0.920 / 0.300 / 0.251).
+// k_query's register budget for the k = 512 batch instance (4 vectors per lane):
+// 48 resident warps per SM (<= 40 registers, no spills with the round-2 scans;
+// c3 / c4 / c5 query phases 0.574 / 0.249 / 0.193 -> 0.538 / 0.241 / 0.187 ms
+// against 40 warps, 0.610 / 0.255 / 0.200 at 32).  (Round 1, per-element
+// accumulators: 40 warps, 48 registers; 48 warps spilled.)
 // k_query_flat's register budget: the 128-thread instances for 56 resident warps
 // per SM (32 registers, a few spilled words), the 32-thread (small-batch)
 // instances for 64 registers as before.  c3 [32, 512] query 0.471 -> 0.428 ms, c3-con
@@ -50,7 +50,7 @@ constexpr int kThreads = 256;
 #define BRMQ_FLAT_WARPS 56
 #endif
 #ifndef BRMQ_QUERY_WARPS
-#define BRMQ_QUERY_WARPS 40
+#define BRMQ_QUERY_WARPS 48
 #endif
 
 struct ElemI32 {
@@ -318,19 +318,24 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
         auto tiny = [&](bool& t, uint64_t lo, uint64_t hi) {
             if (!t || (hi >> 2) - (lo >> 2) > 1) return;
             t = false;
-            const uint64_t v0 = lo >> 2;
+            // 32-bit (value, position) accumulator, strict '<' in position order
+            const uint32_t lo32 = uint32_t(lo), span = uint32_t(hi - lo), p0 = lo32 & ~3u;
+            int32_t bv = 0x7FFFFFFF;
+            uint32_t bi = 0xFFFFFFFFu;
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const uint64_t v = v0 + u;
-                if (v * 4 > hi) break;
-                const int4 x = elem.load_vec(v);
+                const uint32_t p = p0 + 4u * u;
+                if (u == 1 && p > uint32_t(hi)) break;
+                const int4 x = elem.load_vec((lo >> 2) + u);
                 const int32_t e4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                for (int t2 = 0; t2 < 4; ++t2) {
-                    const uint64_t p = v * 4 + t2;
-                    if (p >= lo && p <= hi) best = kmin(best, pack_key(e4[t2], uint32_t(p)));
-                }
+                for (int t2 = 0; t2 < 4; ++t2)
+                    if (p + t2 - lo32 <= span && (e4[t2] < bv || bi == 0xFFFFFFFFu)) {
+                        bv = e4[t2];
+                        bi = p + t2;
+                    }
             }
+            best = kmin(best, pack_key(bv, bi));
         };
         if (elem.scanned) {  // instrumented: cells of every range the rule scans
             uint64_t cells = (t0 ? hi0 - lo0 + 1 : 0) + (t1 ? hi1 - lo1 + 1 : 0);
