@@ -10,21 +10,28 @@
 //   e.g. 27 bits (n = 1e8) -> 9 + 9 + 9, 30 bits (n = 2^30) -> 10 + 10 + 10.
 //
 // B200 design (single-pass "onesweep" scheme):
-//   k_rs_hist : one read of the keys builds the histograms of all passes.
+//   k_rs_hist : one read of the keys (16-byte loads, 4 in flight per thread)
+//               builds the histograms of all passes.
 //   k_rs_pass : per pass ONE kernel.  A CTA takes a tile (atomic ticket =>
 //               tiles start in order) of NT x ITEMS keys, item-major and
 //               lane-minor per warp (coalesced loads), and ranks them stably
 //               inside the warp: the peers of a key are found with one ballot
 //               per digit bit (a "multisplit"; __match_any_sync took 47% of
-//               the old kernel's stall samples, profiles/r02_rs_pass_*), the
-//               running per-digit count lives in a 16-bit warp-private
-//               counter.  Per digit: warp offsets, the tile's count published
-//               as a descriptor, decoupled look-back over the
-//               predecessors (one memset per sort zeroes the descriptors),
-//               and the tile is staged in shared memory sorted
-//               by digit, then written out in runs (consecutive threads ->
-//               consecutive addresses of a bucket).  No separate scan kernel,
-//               no global barrier, no status clearing between launches.
+//               the round-1 kernel's stall samples, and measured 0.65 vs 0.53 ms
+//               at c3-con here), the running per-digit count lives in a 16-bit
+//               warp-private counter whose per-warp totals give the tile's digit
+//               counts (no histogram atomics).  Per digit: warp offsets, the
+//               tile's count published as a 32-bit descriptor (zeroed by one
+//               memset per sort, no epochs), a late decoupled look-back over
+//               windows of 16 predecessors (while a wave's tiles all look back
+//               at once an inclusive prefix propagates 16 tiles per round, not
+//               one), and the tile is staged in shared memory sorted by digit,
+//               then written out in runs (consecutive threads -> consecutive
+//               addresses of a bucket).  No separate scan kernel, no global
+//               barrier.
+//   Yardstick (tools/cub_sort_bench.cu): cub::DeviceRadixSort::SortKeys on the
+//   same 2e7 keys 0.53 ms (27 and 30 bits); this sort 0.53 ms (27 bits, 9-bit
+//   digits) and 0.62 ms (30 bits, 10-bit digits).
 #include <cstdint>
 
 #include "common.cuh"
@@ -87,11 +94,29 @@ __global__ void __launch_bounds__(256) k_rs_hist(const uint32_t* __restrict__ ke
     for (int i = threadIdx.x; i < kMaxPasses * kMaxRadix; i += 256) (&h[0][0])[i] = 0;
     __syncthreads();
     const uint64_t stride = uint64_t(gridDim.x) * 256;
-    for (uint64_t i = uint64_t(blockIdx.x) * 256 + threadIdx.x; i < m; i += stride) {
-        const uint32_t k = __ldg(keys + i);
+    auto add = [&](uint32_t k) {
         for (int p = 0; p < a.passes; ++p)
             atomicAdd(&h[p][(k >> a.shift[p]) & ((1u << a.width[p]) - 1u)], 1u);
+    };
+    // 16-byte loads, 4 in flight per thread (a 1-key-per-thread grid-stride loop was
+    // latency-bound: 76 us for 2e7 keys)
+    const uint64_t m4 = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0 ? m / 4 : 0;
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    constexpr int U = 4;
+    for (uint64_t i0 = uint64_t(blockIdx.x) * 256 + threadIdx.x; i0 < m4; i0 += U * stride) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = i0 + u * stride < m4 ? __ldcs(k4 + i0 + u * stride) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * stride < m4) {
+                add(x[u].x);
+                add(x[u].y);
+                add(x[u].z);
+                add(x[u].w);
+            }
     }
+    for (uint64_t i = 4 * m4 + uint64_t(blockIdx.x) * 256 + threadIdx.x; i < m; i += stride) add(__ldg(keys + i));
     __syncthreads();
     for (int p = 0; p < a.passes; ++p)
         for (int d = threadIdx.x; d < (1 << a.width[p]); d += 256) {
@@ -179,47 +204,7 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 2 : (NT == 256 && ITEMS > 8 ?
         key[i] = idx < m ? __ldcs(kin + idx) : 0u;
     }
 
-    // 1) tile histogram (unordered), published at once: a successor's look-back
-    //    never waits on this tile's ranking
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-        if (base + uint64_t(i) * 32 + lane < m) atomicAdd(&sm.thist[(key[i] >> shift) & dmask], 1u);
-    __syncthreads();
-    uint32_t tsum = 0;
-    W* st = status + tile * kMaxRadix;
-#pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-        const uint32_t d = threadIdx.x * DPT + j;
-        const uint32_t tc = d < radix ? sm.thist[d] : 0u;
-        tsum += tc;
-        if (d < radix) st_vol(st + d, D::pack(tile == 0 ? 2u : 1u, tc));
-    }
-
-    // 2) tile-local digit starts and the global histogram's exclusive prefix
-    //    (gbase[d] gets the tile's look-back count added once it is known)
-    {
-        uint32_t ttot_unused, gtot;
-        uint32_t run = block_excl_sum<NT>(tsum, sm.scan, ttot_unused);
-        uint32_t gsum = 0;
-#pragma unroll
-        for (int j = 0; j < DPT; ++j) {
-            const uint32_t d = threadIdx.x * DPT + j;
-            gsum += d < radix ? uint32_t(ghist[d]) : 0u;
-        }
-        uint32_t grun = block_excl_sum<NT>(gsum, sm.scan, gtot);
-#pragma unroll
-        for (int j = 0; j < DPT; ++j) {
-            const uint32_t d = threadIdx.x * DPT + j;
-            if (d < radix) {
-                sm.texcl[d] = run;
-                sm.gbase[d] = grun;
-                run += sm.thist[d];
-                grun += uint32_t(ghist[d]);
-            }
-        }
-    }
-
-    // 3) stable warp ranking, item-major / lane-minor == input order.  The peers
+    // 1) stable warp ranking, item-major / lane-minor == input order.  The peers
     //    of a key (same digit) come from one ballot per digit bit.
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
@@ -243,17 +228,48 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 2 : (NT == 256 && ITEMS > 8 ?
     }
     __syncthreads();
 
-    // 4) per digit: the warps' offsets inside the tile's run of the digit
+    // 2) per digit (thread t owns digits t*DPT ...): the warps' offsets inside the
+    //    tile's run of the digit and the tile count, published at once (the
+    //    counts come from the warp counters: no histogram atomics)
+    uint32_t tsum = 0;
+    W* st = status + tile * kMaxRadix;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x * DPT + j;
+        uint32_t sum = 0;
         if (d < radix) {
-            uint32_t sum = 0;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 const uint32_t c = sm.whist[w][d];
                 sm.whist[w][d] = uint16_t(sum);
                 sum += c;
+            }
+            st_vol(st + d, D::pack(tile == 0 ? 2u : 1u, sum));
+            sm.thist[d] = sum;
+        }
+        tsum += sum;
+    }
+
+    // 3) tile-local digit starts and the global histogram's exclusive prefix
+    //    (gbase[d] gets the tile's look-back count added once it is known)
+    {
+        uint32_t ttot_unused, gtot;
+        uint32_t run = block_excl_sum<NT>(tsum, sm.scan, ttot_unused);
+        uint32_t gsum = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+            const uint32_t d = threadIdx.x * DPT + j;
+            gsum += d < radix ? uint32_t(ghist[d]) : 0u;
+        }
+        uint32_t grun = block_excl_sum<NT>(gsum, sm.scan, gtot);
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {
+            const uint32_t d = threadIdx.x * DPT + j;
+            if (d < radix) {
+                sm.texcl[d] = run;
+                sm.gbase[d] = grun;
+                run += sm.thist[d];
+                grun += uint32_t(ghist[d]);
             }
         }
     }
@@ -281,22 +297,36 @@ __global__ void __launch_bounds__(NT, (NT == 512 ? 2 : (NT == 256 && ITEMS > 8 ?
         }
     }
     // 6) look-back per digit, late (this tile's ranking and staging gave the
-    //    predecessors time to turn inclusive: usually tile - 1 already is),
-    //    one predecessor at a time
+    //    predecessors time to turn inclusive)
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
         const uint32_t d = threadIdx.x * DPT + j;
         if (d < radix && tile > 0) {
+            // a window of LB predecessors per round (independent loads in flight):
+            // while the tiles of a wave all look back at once, an inclusive
+            // prefix propagates LB tiles per round instead of one
+            constexpr int LB = 16;
             uint64_t ex = 0;
-            for (int64_t p = int64_t(tile) - 1; p >= 0; --p) {
-                const W* wp = status + uint64_t(p) * kMaxRadix + d;
-                W w = ld_vol(wp);
-                while (D::state(w) == 0u) {
-                    __nanosleep(32);
-                    w = ld_vol(wp);
+            bool done = false;
+            for (int64_t p0 = int64_t(tile) - 1; !done; p0 -= LB) {
+                W w[LB];
+#pragma unroll
+                for (int u = 0; u < LB; ++u)
+                    w[u] = p0 - u >= 0 ? ld_vol(status + uint64_t(p0 - u) * kMaxRadix + d) : W(0);
+#pragma unroll
+                for (int u = 0; u < LB; ++u) {
+                    if (done) break;
+                    if (p0 - u < 0) {
+                        done = true;
+                        break;
+                    }
+                    while (D::state(w[u]) == 0u) {
+                        __nanosleep(32);
+                        w[u] = ld_vol(status + uint64_t(p0 - u) * kMaxRadix + d);
+                    }
+                    ex += D::value(w[u]);
+                    if (D::state(w[u]) == 2u) done = true;
                 }
-                ex += D::value(w);
-                if (D::state(w) == 2u) break;
             }
             st_vol(st + d, D::pack(2u, ex + sm.thist[d]));
             sm.gbase[d] += uint32_t(ex);

@@ -68,6 +68,25 @@ int main(int argc, char** argv) {
             sum += ms;
         }
     }
+    // keys only (the solve pipeline sorts the endpoint positions alone)
+    size_t tmp_k = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_k, k0, k1, int64_t(m), 0, bits));
+    void* tmpk;
+    CK(cudaMalloc(&tmpk, tmp_k));
+    double best_k = 1e30;
+    for (int r = 0; r < reps + 2; ++r) {
+        CK(cudaMemcpy(k0, hk.data(), m * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(flush, r, 256u << 20));
+        cudaEventRecord(a);
+        CK(cub::DeviceRadixSort::SortKeys(tmpk, tmp_k, k0, k1, int64_t(m), 0, bits));
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (r >= 2) best_k = ms < best_k ? ms : best_k;
+    }
+    std::printf("{\"tool\": \"cub::DeviceRadixSort::SortKeys\", \"m\": %llu, \"bits\": %d, \"ms_best\": %.4f}\n",
+                (unsigned long long)m, bits, best_k);
     std::vector<uint32_t> ok(m);
     CK(cudaMemcpy(ok.data(), k1, m * 4, cudaMemcpyDeviceToHost));
     bool sorted = true;
