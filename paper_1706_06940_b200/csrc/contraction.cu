@@ -57,6 +57,9 @@ constexpr int kRow = 32;            // positions per lane = one 128-byte row
 constexpr int kWTile = 32 * kRow;   // 1024 positions = 4 KB per warp tile
 constexpr int kTile = 4 * kWTile;   // 4096: the partition unit
 static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
+#ifndef BRMQ_CHUNKED_DENSE
+#define BRMQ_CHUNKED_DENSE 1  // dense rows skip boundary-free chunk columns (instance with the sparse path)
+#endif
 #ifndef BRMQ_KDENSE
 #define BRMQ_KDENSE 2
 #endif
@@ -255,7 +258,12 @@ __device__ __forceinline__ void row_pass_all(const RW& rw, uint32_t r, uint32_t 
 // element (BSSY/BRA/BSYNC around every compare), this one 8.
 constexpr int kCap = 16;  // capture slots per lane
 constexpr size_t kCapSmem = size_t(NW) * kCap * 32 * 8;  // dynamic shared memory of k_contract
-template <bool MARKED, bool FUSE, class RW>
+// CHUNKED (the instance with the sparse path, few boundaries per dense tile): a
+// 16-byte chunk in which no lane of the warp has a boundary is folded with one
+// 3-way minimum and a leftmost-index select (~10 instructions instead of ~36);
+// the per-element walk runs only for chunk columns where some lane has one
+// (warp-uniform test, no divergence).
+template <bool MARKED, bool FUSE, class RW, bool CHUNKED = false>
 __device__ __forceinline__ void row_pass_cap(const RW& rw, uint32_t r, uint32_t fl, uint64_t rank,
                                              const AqOut& aq, uint64_t& hp, uint64_t& run,
                                              uint32_t cap /* shared address of slot 0 of this lane */) {
@@ -266,6 +274,15 @@ __device__ __forceinline__ void row_pass_cap(const RW& rw, uint32_t r, uint32_t 
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
         const int4 x = rw.chunk(r, c);
+        if (CHUNKED && !__any_sync(kFull, ((fl >> (4 * c)) & 0xFu) != 0u)) {
+            const int32_t m = __vimin3_s32(x.x, x.y, min(x.z, x.w));
+            const uint32_t e = x.x == m ? 0u : x.y == m ? 1u : x.z == m ? 2u : 3u;
+            if (m < rv) {  // strict: the earlier position keeps ties
+                rv = m;
+                ri = uint32_t(4 * c) + e;
+            }
+            continue;
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t j = uint32_t(4 * c + e);
@@ -588,7 +605,7 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
             uint64_t hp = kNoKey;
             if (!GEN) {
                 if (!__any_sync(kFull, __popc(fl) > kCap))
-                    row_pass_cap<MARKED, FUSE>(rs, lane, fl, rank, out, hp, run,
+                    row_pass_cap<MARKED, FUSE, Rows, SPARSE && BRMQ_CHUNKED_DENSE>(rs, lane, fl, rank, out, hp, run,
                                          smem_u32(s_cap) + (warp * kCap * 32u + lane) * 8u);
                 else
                     row_pass_all<MARKED, FUSE>(rs, lane, fl, rank, out, hp, run);
