@@ -504,6 +504,11 @@ __global__ void k_publish(const uint32_t* __restrict__ ctl, uint32_t* __restrict
     __threadfence_system();
 }
 
+brmq::CtlPublish publish_ctl(brmq_ctx* c, Control* ctl) {
+    return brmq::CtlPublish{reinterpret_cast<const uint32_t*>(ctl), c->ctl_host_dev, nullptr,
+                            uint32_t(kCtlHeader / 4), uint32_t(offsetof(Control, nb) / 4)};
+}
+
 int publish(brmq_ctx* c, Control* ctl, cudaStream_t s) {
     brmq::launch_k(k_publish, dim3(1), dim3(32), 0, s, reinterpret_cast<const uint32_t*>(ctl),
                    c->ctl_host_dev, uint32_t(kCtlHeader / 4), uint32_t(offsetof(Control, nb) / 4));
@@ -1115,15 +1120,16 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         tm.end(l);
         tm.stage("query", launches);
         const uint2* wi = reinterpret_cast<uint2*>(P(i_wi));
+        // the query kernel writes nothing into the control header: its first warp
+        // publishes it (publish_early), no k_publish launch
         if (sub_level)
             l = brmq::launch_query_con_flat(AQ, k, ST, b_max, SUB, dQ, wi, nullptr, nullptr, n, q, dAns, s,
-                                            brmq::CtlPublish{});
+                                            publish_ctl(c, ctl));
         else
             l = brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ, wi, n, q, dAns, s,
-                                                 brmq::CtlPublish{});
+                                                 publish_ctl(c, ctl));
         launches += l;
         tm.end(l);
-        launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);

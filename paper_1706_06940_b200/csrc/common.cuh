@@ -124,4 +124,16 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
     return r;
 }
 
+// Publication of the control header by the final kernel of a solve whose final
+// kernel writes nothing into the header itself (BbST_CON): every earlier kernel
+// has completed (stream order), so the first warp of CTA 0 copies the header to
+// the host-mapped mirror at once and re-zeroes the accumulating fields for the
+// next solve -- no tail launch (k_publish: ~3 us per solve at c2).
+__device__ __forceinline__ void publish_early(const CtlPublish& p) {
+    if (!p.host || blockIdx.x != 0 || threadIdx.x >= 32) return;
+    for (uint32_t i = threadIdx.x; i < p.words; i += 32) p.host[i] = __ldcg(p.ctl + i);
+    __syncwarp();
+    for (uint32_t i = threadIdx.x; i < p.reset_words; i += 32) const_cast<uint32_t*>(p.ctl)[i] = 0u;
+}
+
 }  // namespace brmq

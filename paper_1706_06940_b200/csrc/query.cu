@@ -272,6 +272,7 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
                                               uint64_t stride, uint64_t q,
                                               uint64_t* __restrict__ answers,
                                               const CtlPublish pub) {
+    publish_early(pub);  // (BbST_CON only: the BbST callers pass no publication)
     // the vectorised instances know k at compile time (k = 32 * EPV * VPL): block
     // indices by shifts, not 64-bit divisions
     const uint32_t k = VPL > 0 ? uint32_t(32 * E::EPV * (VPL > 0 ? VPL : 1)) : k_rt;
@@ -972,6 +973,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 32)) k_
                                                    uint64_t* __restrict__ answers,
                                                    const CtlPublish pub) {
     brmq::pdl_wait();
+    publish_early(pub);
     constexpr int kRowCap = 64;  // <= 2 rows per lane
     __shared__ uint4 s_rows[NT / 32][kRowCap];
     const uint32_t warp = threadIdx.x >> 5;
