@@ -593,8 +593,8 @@ int solve_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint64_t offset
     if (!dev) {
         auto* hA = reinterpret_cast<int32_t*>(buf + ((q * 33 + 64 + 15) & ~size_t(15)));
         auto* hQ = reinterpret_cast<ulonglong2*>(reinterpret_cast<char*>(hA) + a_bytes);
-        CUDA_TRY(c->stager.h2d(hA, A, n_shard * 4, s));
         CUDA_TRY(c->stager.h2d(hQ, Q, q * 16, s));
+        CUDA_TRY(c->stager.h2d(hA, A, n_shard * 4, s));
         dA = hA;
         dQ = hQ;
     }
@@ -679,8 +679,8 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("query", launches);
@@ -749,8 +749,8 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -839,8 +839,8 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         int l = 0;
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -931,8 +931,8 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         tm.stage("block_argmin", launches);
@@ -1056,8 +1056,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         // the epochs of this solve are reserved by the first kernel (k_collect)
@@ -1224,8 +1224,8 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
         // (the control header is zeroed by the previous solve's final kernel, see prepare_ctl)
         if (!dev) {
             tm.stage("h2d", launches);
+            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));  // small first: A's DMA runs last
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
-            CUDA_TRY(c->stager.h2d(const_cast<uint64_t*>(dQ), Q, q * 16, s));
             tm.end(0);
         }
         // the epochs of this solve are reserved by the first kernel (k_collect)
