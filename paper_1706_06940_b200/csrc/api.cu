@@ -109,6 +109,7 @@ struct brmq_ctx {
     bool use_graphs = true;
     bool use_pdl = false;  // programmatic dependent launches inside a solve (BRMQ_PDL=1: on; DESIGN 3.5)
     bool count_scans = false;  // brmq_ctx_set_counters
+    bool use_msd = true;  // radix pipeline: MSD partition + bucket marks (BRMQ_MSD=0: LSD over all digits)
     // small A_Q: block / sub-block minima by reductions inside the contraction
     // (BRMQ_FUSE=1: on).  Off: measured -1 us at c2 in one harness and +16 us in
     // bench.py's process (DESIGN 3.1)
@@ -407,6 +408,7 @@ int brmq_ctx_create(brmq_ctx** out, int device) {
     if (const char* g = getenv("BRMQ_GRAPHS")) c->use_graphs = atoi(g) != 0;
     if (const char* g = getenv("BRMQ_PDL")) c->use_pdl = atoi(g) != 0;
     if (const char* g = getenv("BRMQ_FUSE")) c->use_fuse = atoi(g) != 0;
+    if (const char* g = getenv("BRMQ_MSD")) c->use_msd = atoi(g) != 0;
     *out = c;
     return BRMQ_OK;
 }
@@ -1077,24 +1079,44 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         } else {
             auto* k0 = reinterpret_cast<uint32_t*>(P(i_k0));
             auto* k1 = reinterpret_cast<uint32_t*>(P(i_k1));
+            // MSD (radix_partition_shape): the collect builds the top-digit
+            // histogram; a partition pass, then per bucket a counting digit in
+            // shared memory that dedups and marks the bitmap
+            const uint64_t bm_words = brmq::contract_bitmap_words(n);
+            int D = 0, Lb = 0;
+            const bool msd = c->use_msd && brmq::radix_partition_shape(bits, m, bm_words, &D, &Lb);
+            if (msd) CUDA_TRY(cudaMemsetAsync(P(i_rs), 0, brmq::radix_sort_temp_bytes(m, bits), s));
             tm.stage("collect", launches);
-            l = brmq::launch_collect(dQ, q, n, k0, nullptr, nullptr, nullptr, &ctl->err, s,
-                                     c->epoch_dev, n_epochs, fill0, fill0_n, fill1, fill1_n);
+            l = brmq::launch_collect(dQ, q, n, k0, nullptr, nullptr, msd ? ctl->span : nullptr, &ctl->err, s,
+                                     c->epoch_dev, n_epochs, fill0, fill0_n, fill1, fill1_n,
+                                     msd ? brmq::radix_partition_hist(P(i_rs)) : nullptr, uint32_t(Lb),
+                                     msd ? (1u << D) - 1u : 0u);
             launches += l;
             tm.end(l);
             tm.stage("radix_sort", launches);
-            bool in_alt = false;
-            l = brmq::launch_radix_sort(k0, nullptr, k1, nullptr, m, bits, P(i_rs), S(i_rst), s, &in_alt,
-                                        c->epoch_dev, 2);
-            launches += l;
-            tm.end(l);
-            // dedup: the sorted positions mark the bitmap (coalesced, no look-back);
-            // ranks per contraction piece from the bitmap as in the bitmap pipeline
-            tm.stage("unique_rank", launches);
-            l = brmq::launch_mark_sorted(in_alt ? k1 : k0, m, n, c->bitmap, ctl->span, &ctl->err, s);
-            l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
-            launches += l;
-            tm.end(l);
+            if (msd) {
+                l = brmq::launch_radix_partition_mark(k0, k1, m, bits, n, P(i_rs), c->bitmap, bm_words, &ctl->err,
+                                                      s);
+                launches += l;
+                tm.end(l);
+                tm.stage("unique_rank", launches);
+                l = brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
+                launches += l;
+                tm.end(l);
+            } else {  // LSD over all digits
+                bool in_alt = false;
+                l = brmq::launch_radix_sort(k0, nullptr, k1, nullptr, m, bits, P(i_rs), S(i_rst), s, &in_alt,
+                                            c->epoch_dev, 2);
+                launches += l;
+                tm.end(l);
+                // dedup: the sorted positions mark the bitmap (coalesced, no look-back);
+                // ranks per contraction piece from the bitmap as in the bitmap pipeline
+                tm.stage("unique_rank", launches);
+                l = brmq::launch_mark_sorted(in_alt ? k1 : k0, m, n, c->bitmap, ctl->span, &ctl->err, s);
+                l += brmq::launch_piece_count(c->bitmap, ctl->span, n, pcnt, ctl->rcnt, s);
+                launches += l;
+                tm.end(l);
+            }
         }
         tm.stage("contract", launches);
         const brmq::ContractFuse fz{SUB, ST, b_max, brmq::floor_log2_u64(k), &ctl->b_dev};

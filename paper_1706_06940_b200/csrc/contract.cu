@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
                                                       uint32_t epoch_by, uint32_t mark_lo,
                                                       uint32_t mark_hi, uint64_t* __restrict__ fill0,
                                                       uint64_t fill0_n, uint64_t* __restrict__ fill1,
-                                                      uint64_t fill1_n) {
+                                                      uint64_t fill1_n,
+                                                      unsigned long long* __restrict__ hist,
+                                                      uint32_t hshift, uint32_t hmask) {
     brmq::pdl_wait();
     brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     {
@@ -57,7 +59,10 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
     // the solve's epoch reservation rides on this first kernel (no extra launch)
     if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) *epoch_bump += epoch_by;
     __shared__ uint32_t s_lo, s_hi;
+    __shared__ uint32_t s_hist[1024];  // hist: the radix partition's top-digit counts
     if (threadIdx.x == 0) { s_lo = 0xFFFFFFFFu; s_hi = 0; }
+    if (hist)
+        for (uint32_t d = threadIdx.x; d <= hmask; d += kThreads) s_hist[d] = 0;
     __syncthreads();
     uint32_t lo_acc = 0xFFFFFFFFu, hi_acc = 0;
     const uint64_t stride = uint64_t(gridDim.x) * kThreads;
@@ -86,6 +91,10 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
         if (vals)
             reinterpret_cast<uint2*>(vals)[i] =
                 make_uint2(uint32_t(i << 1), uint32_t((i << 1) | 1u));  // contraction.hpp:16-18
+        if (hist) {
+            atomicAdd(&s_hist[(lo >> hshift) & hmask], 1u);
+            atomicAdd(&s_hist[(hi >> hshift) & hmask], 1u);
+        }
         if (bitmap) {  // only the endpoints in this pass's slice [mark_lo, mark_hi]
             if (lo - mark_lo <= mark_hi - mark_lo) atomicOr(bitmap + (lo >> 5), 1u << (lo & 31));
             if (hi - mark_lo <= mark_hi - mark_lo) atomicOr(bitmap + (hi >> 5), 1u << (hi & 31));
@@ -106,6 +115,11 @@ __global__ void __launch_bounds__(kThreads) k_collect(const ulonglong2* __restri
             atomicMax(span + 0, ~s_lo);
             atomicMax(span + 1, s_hi);
         }
+    }
+    if (hist) {
+        __syncthreads();
+        for (uint32_t d = threadIdx.x; d <= hmask; d += kThreads)
+            if (const uint32_t c = s_hist[d]) atomicAdd(hist + d, (unsigned long long)c);
     }
 }
 
@@ -491,8 +505,10 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump, uint32_t epoch_by, uint64_t* fill0, uint64_t fill0_n,
-                   uint64_t* fill1, uint64_t fill1_n) {
+                   uint64_t* fill1, uint64_t fill1_n, unsigned long long* hist, uint32_t hshift,
+                   uint32_t hmask) {
     if (q == 0) return 0;
+    if (hist && hmask >= 1024u) return -1;
     // small batches: one CTA per SM (fewer span atomics, c2 -1.3 us); large ones
     // need the wide grid for the loads in flight (c5 at 148 CTAs: 0.25 -> 0.70 ms)
     const unsigned cap = q <= (uint64_t(1) << 18) ? 148u : 148u * 16u;
@@ -509,7 +525,7 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
     if (slices <= 1) {
         brmq::launch_k(k_collect, dim3(grid), dim3(kThreads), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
                                                bitmap, span, err, epoch_bump, epoch_by, 0u, ~0u,
-                                               fill0, fill0_n, fill1, fill1_n);
+                                               fill0, fill0_n, fill1, fill1_n, hist, hshift, hmask);
         return 1;
     }
     const uint64_t per = (n + slices - 1) / slices;
@@ -519,7 +535,8 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
                                                bitmap, span, err, t == 0 ? epoch_bump : nullptr,
                                                epoch_by, uint32_t(a), uint32_t(b - 1),
                                                t == 0 ? fill0 : nullptr, t == 0 ? fill0_n : 0,
-                                               t == 0 ? fill1 : nullptr, t == 0 ? fill1_n : 0);
+                                               t == 0 ? fill1 : nullptr, t == 0 ? fill1_n : 0,
+                                               t == 0 ? hist : nullptr, hshift, hmask);
     }
     return int(slices);
 }

@@ -146,6 +146,20 @@ int radix_sort_passes(int bits);
 int launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* alt_keys, uint32_t* alt_vals,
                       uint64_t m, int bits, void* tmp, uint64_t* status, cudaStream_t stream,
                       bool* result_in_alt, const uint32_t* epoch_dev, uint32_t epoch_off);
+// The radix pipeline's sort + dedup as a two-level MSD radix sort: keys of 8..30
+// bits, m >= 2^14 (radix_partition_shape; false: sort LSD with launch_radix_sort).
+//   1. cudaMemsetAsync(tmp, 0, radix_sort_temp_bytes(m, bits))
+//   2. launch_collect(..., span, ..., hist = radix_partition_hist(tmp), hshift = L,
+//      hmask = 2^D - 1): the span and the top-digit histogram
+//   3. launch_radix_partition_mark: the keys partitioned by their top D bits into
+//      alt_keys (unstable: bucket order is all the next level needs), then per
+//      bucket a counting digit over the low L bits in shared memory that dedups
+//      and marks the (all-zero) boundary bitmap; err bit 2 as launch_mark_sorted.
+bool radix_partition_shape(int bits, uint64_t m, uint64_t bitmap_words, int* D, int* L);
+unsigned long long* radix_partition_hist(void* tmp);
+int launch_radix_partition_mark(const uint32_t* keys, uint32_t* alt_keys, uint64_t m, int bits, uint64_t n,
+                                void* tmp, uint32_t* bitmap, uint64_t bitmap_words, uint32_t* err,
+                                cudaStream_t stream);
 
 // ---------------------------------------------------------------- contract.cu
 // The contraction partitions the tiles of A into G ranges of R tiles
@@ -162,7 +176,8 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0,
                    uint64_t* fill0 = nullptr, uint64_t fill0_n = 0, uint64_t* fill1 = nullptr,
-                   uint64_t fill1_n = 0);
+                   uint64_t fill1_n = 0, unsigned long long* hist = nullptr, uint32_t hshift = 0,
+                   uint32_t hmask = 0);
 // Boundaries per contraction piece (pcnt[g * 8 + w], 8 warps per range) and per
 // range (rcnt[g]), popcounted from the bitmap.
 #ifndef BRMQ_CWARPS

@@ -31,7 +31,17 @@
 //               barrier.
 //   Yardstick (tools/cub_sort_bench.cu): cub::DeviceRadixSort::SortKeys on the
 //   same 2e7 keys 0.53 ms (27 and 30 bits); this sort 0.53 ms (27 bits, 9-bit
-//   digits) and 0.62 ms (30 bits, 10-bit digits).
+//   digits) and 0.62 ms (30 bits, 10-bit digits).  It serves the stage API's
+//   (pos, origin) pairs, ST-RMQ_CON and keys wider than 30 bits.
+//
+// The BbST_CON radix pipeline's sort + dedup is a two-level MSD radix sort
+// instead (launch_radix_partition_mark): the collect kernel counts the top D
+// bits, k_msd_partition scatters the keys by them (shared-atomic ranks, one
+// global reservation per tile and digit -- no look-back, no stability needed),
+// and k_bucket_mark finishes each bucket with a counting digit over the low L
+// bits in shared memory, which also dedups and marks the boundary bitmap the
+// contraction reads.  c3-con (2e7 endpoints, 27 bits): sort + dedup 0.57 ->
+// 0.10 ms (+ ~12 us of histogram in the collect); c5-con (30 bits) 0.74 -> 0.15 ms.
 #include <cstdint>
 
 #include "common.cuh"
@@ -388,7 +398,203 @@ void launch_pass_w(uint64_t tiles, const uint32_t* kin, const uint32_t* vin, uin
     }
 }
 
+// MSD partition pass: tile of NT x ITEMS keys; the rank of a key inside its
+// digit comes from a shared atomic on the tile's digit counter (the bucket
+// order is all the next level needs, so no stable ranking), the tile's run of
+// each digit is reserved with one global atomic on the digit's counter past the
+// digit's start (the exclusive prefix of the collect-time histogram) -- no
+// look-back chain -- and the tile is staged sorted by digit and written in runs.
+#ifndef BRMQ_PART_NT
+#define BRMQ_PART_NT 512
+#endif
+#ifndef BRMQ_PART_ITEMS
+#define BRMQ_PART_ITEMS 16
+#endif
+#ifndef BRMQ_PART_MINB
+#define BRMQ_PART_MINB 1
+#endif
+constexpr int kNtPart = BRMQ_PART_NT, kItemsPart = BRMQ_PART_ITEMS;
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT, (NT == kNtPart ? BRMQ_PART_MINB : 1)) k_msd_partition(const uint32_t* __restrict__ kin,
+                                                      uint32_t* __restrict__ kout, uint64_t m, int shift,
+                                                      uint32_t dmask,
+                                                      const unsigned long long* __restrict__ ghist,
+                                                      uint32_t* __restrict__ gcnt,
+                                                      uint32_t* __restrict__ bstart) {
+    brmq::pdl_wait();
+    constexpr int NW = NT / 32, TILE = NT * ITEMS, DPT = kMaxRadix / NT;
+    static_assert(TILE <= 65536, "16-bit ranks");
+    __shared__ uint32_t th[kMaxRadix], texcl[kMaxRadix], base[kMaxRadix];
+    __shared__ uint32_t scan[NW + 1];
+    __shared__ uint32_t skey[TILE];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kMaxRadix; i += NT) th[i] = 0u;
+    __syncthreads();
+    const uint64_t tbase = uint64_t(blockIdx.x) * TILE;
+    const uint64_t wbase = tbase + uint64_t(warp) * (32 * ITEMS);
+    uint32_t key[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const uint64_t idx = wbase + uint64_t(i) * 32 + lane;
+        key[i] = idx < m ? __ldcs(kin + idx) : 0u;
+    }
+    uint32_t rk2[(ITEMS + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = wbase + uint64_t(i) * 32 + lane < m;
+        const uint32_t r = ok ? atomicAdd(&th[(key[i] >> shift) & dmask], 1u) : 0u;
+        rk2[i / 2] = (i & 1) ? (rk2[i / 2] | (r << 16)) : r;
+    }
+    __syncthreads();
+    // reservations first: their latency overlaps the two block scans
+    uint32_t tsum = 0, gsum = 0, c[DPT], got[DPT], gh[DPT];
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x * DPT + j;
+        c[j] = th[d];
+        got[j] = c[j] ? atomicAdd(gcnt + d, c[j]) : 0u;
+        gh[j] = d <= dmask ? uint32_t(ghist[d]) : 0u;
+        tsum += c[j];
+        gsum += gh[j];
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_sum<NT>(tsum, scan, tot);
+    uint32_t grun = block_excl_sum<NT>(gsum, scan, tot);
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const uint32_t d = threadIdx.x * DPT + j;
+        texcl[d] = run;
+        if (c[j]) base[d] = grun + got[j];
+        if (blockIdx.x == 0) bstart[d] = grun;  // the buckets' starts, for k_bucket_mark
+        run += c[j];
+        grun += gh[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        if (wbase + uint64_t(i) * 32 + lane < m) {
+            const uint32_t d = (key[i] >> shift) & dmask;
+            skey[texcl[d] + ((rk2[i / 2] >> (16 * (i & 1))) & 0xFFFFu)] = key[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t ttot = uint32_t(m - tbase < uint64_t(TILE) ? m - tbase : uint64_t(TILE));
+    for (uint32_t s = threadIdx.x; s < ttot; s += NT) {
+        const uint32_t k = skey[s];
+        const uint32_t d = (k >> shift) & dmask;
+        kout[base[d] + (s - texcl[d])] = k;
+    }
+}
+
+// MSD partition + per-bucket marking (launch_radix_partition_mark): bucket b of
+// the top-digit partition holds exactly the keys in [b << L, (b + 1) << L); its
+// CTA sorts and dedups them by one counting digit of L bits -- a presence bitmap
+// of 2^L bits in shared memory, set by shared atomics -- and writes the bucket's
+// nonzero bitmap words (the global bitmap is all-zero on entry: the contraction
+// clears every word it consumes); err bit 2 for positions >= n.
+#ifndef BRMQ_MARK_U
+#define BRMQ_MARK_U 8
+#endif
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bucket_mark(
+    const uint32_t* __restrict__ keys, uint64_t n, int L, const unsigned long long* __restrict__ ghist,
+    const uint32_t* __restrict__ bstart, uint32_t* __restrict__ bitmap, uint64_t bitmap_words,
+    uint32_t* __restrict__ err) {
+    brmq::pdl_wait();
+    constexpr int kMarkThreads = NT;
+    extern __shared__ __align__(16) uint32_t bm[];
+    const uint32_t b = blockIdx.x;
+    const uint64_t cnt = ghist[b];
+    if (cnt == 0) return;  // nothing to mark: the bucket's words stay zero
+    const uint32_t nw = 1u << (L - 5);  // bitmap words of the bucket (L >= 7)
+    for (uint32_t w = threadIdx.x * 4; w < nw; w += kMarkThreads * 4)
+        *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const uint64_t start = bstart[b], lo = uint64_t(b) << L;
+    uint32_t bad = 0;
+    constexpr int U = BRMQ_MARK_U;
+    for (uint64_t i0 = threadIdx.x; i0 < cnt; i0 += U * kMarkThreads) {
+        uint32_t x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = i0 + u * kMarkThreads < cnt ? __ldcs(keys + start + i0 + u * kMarkThreads) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (i0 + u * kMarkThreads >= cnt) break;
+            if (x[u] >= n) {
+                bad = 2u;
+                continue;
+            }
+            const uint32_t r = uint32_t(x[u] - lo);
+            atomicOr(bm + (r >> 5), 1u << (r & 31));
+        }
+    }
+    if (bad) atomicOr(err, bad);
+    __syncthreads();
+    const uint64_t w0 = lo >> 5;
+    for (uint32_t w = threadIdx.x * 4; w < nw; w += kMarkThreads * 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(bm + w);
+        if ((v.x | v.y | v.z | v.w) == 0u) continue;
+        if (w0 + w + 4 <= bitmap_words) {
+            *reinterpret_cast<uint4*>(bitmap + w0 + w) = v;
+        } else {
+            const uint32_t e[4] = {v.x, v.y, v.z, v.w};
+            for (int j = 0; j < 4; ++j)
+                if (w0 + w + j < bitmap_words && e[j]) bitmap[w0 + w + j] = e[j];
+        }
+    }
+}
+
 }  // namespace
+
+bool radix_partition_shape(int bits, uint64_t m, uint64_t bitmap_words, int* D, int* L) {
+    // small batches keep the LSD passes (c1, m = 2e3: 0.022 vs 0.028 ms)
+    if (bits < 8 || bits > 30 || m < (1u << 14) || m >= (uint64_t(1) << 32) || (bitmap_words & 3u)) return false;
+    *D = bits - 7 < kMaxBits ? bits - 7 : kMaxBits;
+    *L = bits - *D;
+    return *L <= 20;
+}
+
+unsigned long long* radix_partition_hist(void* tmp) { return static_cast<unsigned long long*>(tmp); }
+
+// The partitioned keys land in alt_keys; the top-digit histogram is in tmp[0..),
+// the reservation counters (zeroed with it) at tmp + 8 KB, the buckets' starts
+// at tmp + 12 KB.
+int launch_radix_partition_mark(const uint32_t* keys, uint32_t* alt_keys, uint64_t m, int bits, uint64_t n,
+                                void* tmp, uint32_t* bitmap, uint64_t bitmap_words, uint32_t* err,
+                                cudaStream_t stream) {
+    int D = 0, L = 0;
+    if (!radix_partition_shape(bits, m, bitmap_words, &D, &L)) return -1;
+    const auto* ghist = static_cast<const unsigned long long*>(tmp);
+    auto* gcnt = reinterpret_cast<uint32_t*>(static_cast<char*>(tmp) + kMaxRadix * 8);
+    auto* bstart = gcnt + kMaxRadix;
+    if (m <= kSmallM) {
+        constexpr int T = kNtSmall * kItemsSmall;
+        brmq::launch_k(k_msd_partition<kNtSmall, kItemsSmall>, dim3(unsigned((m + T - 1) / T)), dim3(kNtSmall), 0,
+                       stream, keys, alt_keys, m, L, (1u << D) - 1u, ghist, gcnt, bstart);
+    } else {
+        constexpr int T = kNtPart * kItemsPart;
+        brmq::launch_k(k_msd_partition<kNtPart, kItemsPart>, dim3(unsigned((m + T - 1) / T)), dim3(kNtPart), 0,
+                       stream, keys, alt_keys, m, L, (1u << D) - 1u, ghist, gcnt, bstart);
+    }
+    // 1024 threads for the largest buckets (L >= 18: 32 KB+ of bitmap, 1 CTA per
+    // SM at L = 20), 512 below (c3-con: 0.120 -> 0.108 ms partition + marks)
+    const size_t smem = size_t(1u << (L - 5)) * 4;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+        cudaFuncSetAttribute(k_bucket_mark<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+        cudaFuncSetAttribute(k_bucket_mark<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+        attr[dev & 63] = true;
+    }
+    if (L >= 18)
+        brmq::launch_k(k_bucket_mark<1024>, dim3(1u << D), dim3(1024), smem, stream, alt_keys, n, L, ghist, bstart,
+                       bitmap, bitmap_words, err);
+    else
+        brmq::launch_k(k_bucket_mark<512>, dim3(1u << D), dim3(512), smem, stream, alt_keys, n, L, ghist, bstart,
+                       bitmap, bitmap_words, err);
+    return 2;
+}
 
 // [ghist: 4 x 1024 u64][tickets: 4 u32 padded to 256 B], zeroed by every sort
 size_t radix_sort_temp_bytes(uint64_t, int) { return size_t(kMaxPasses * kMaxRadix * 8) + 256; }

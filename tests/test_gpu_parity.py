@@ -554,3 +554,35 @@ def test_scan_counter_matches_oracle(engine, orc):
         assert info["scanned_cells"] == S_dev, (n, q, info["scanned_cells"], S, S_dev)
     engine.solve_batch_bbst(A, Q, 512)
     assert engine.solve_info()["scanned_cells"] == 0  # off again
+
+
+@pytest.mark.parametrize("n", [130, 1000, 4097, 65_541, (1 << 20) + 3, 3_000_001])
+def test_radix_msd_partition(engine, orc, n):
+    """The radix pipeline's two-level sort + dedup (radix_sort.cu
+    launch_radix_partition_mark: an MSD partition by the top digit, then a
+    counting digit per bucket in shared memory), used from 2^14 endpoints: key
+    widths 8..22 bits, n just above a power of two (the last bucket runs past
+    the bitmap), every endpoint inside one bucket, heavy duplicates, and the
+    out-of-range error -- against the oracle and the bitmap pipeline."""
+    r = np.random.default_rng(n)
+    A = _values(r, n, "ties16" if n % 2 else "uniform")
+    q = 12_000
+    cases = [_queries(r, n, q, "uniform"), _queries(r, n, q, "short")]
+    lo = n // 3
+    a = r.integers(lo, min(n, lo + 100), q)  # one bucket (or two) holds every endpoint
+    b = np.minimum(a + r.integers(0, 60, q), n - 1)
+    cases.append(np.stack([np.minimum(a, b), np.maximum(a, b)], 1).astype(np.uint64))
+    cases.append(np.tile(np.array([[lo, n - 1]], np.uint64), (q, 1)))  # 2q copies of two keys
+    for Q in cases:
+        want = orc.solve_oracle(A, Q)
+        for kind in (SortKind.Radix, SortKind.Bitmap):
+            for k in (8, 512):
+                got = engine.solve_batch_bbst_con(A, Q, k, kind)
+                bad = np.nonzero(got != want)[0]
+                assert bad.size == 0, (n, kind, k, bad[:5])
+    Q = _queries(r, n, q, "uniform")
+    Q[q // 2, 1] = n  # out of range -> std::out_of_range (naive.hpp:14-15)
+    with pytest.raises(OutOfRange):
+        engine.solve_batch_bbst_con(A, Q, 512, SortKind.Radix)
+    assert list(engine.solve_batch_bbst_con(A, make_queries([0], [n - 1]), 512, SortKind.Radix)) == \
+        list(orc.solve_oracle(A, make_queries([0], [n - 1])))
