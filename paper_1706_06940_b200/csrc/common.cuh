@@ -135,5 +135,4 @@ __device__ __forceinline__ void publish_early(const CtlPublish& p) {
     __syncwarp();
     for (uint32_t i = threadIdx.x; i < p.reset_words; i += 32) const_cast<uint32_t*>(p.ctl)[i] = 0u;
 }
-
 }  // namespace brmq

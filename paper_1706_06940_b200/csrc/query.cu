@@ -49,6 +49,9 @@ constexpr int kThreads = 256;
 #ifndef BRMQ_FLAT_WARPS
 #define BRMQ_FLAT_WARPS 56
 #endif
+#ifndef BRMQ_TINY_VECS
+#define BRMQ_TINY_VECS 2  // ranges within this many 16-byte vectors: scanned lane-private
+#endif
 #ifndef BRMQ_QUERY_WARPS
 #define BRMQ_QUERY_WARPS 48
 #endif
@@ -272,7 +275,10 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
                                               uint64_t stride, uint64_t q,
                                               uint64_t* __restrict__ answers,
                                               const CtlPublish pub) {
-    publish_early(pub);  // (BbST_CON only: the BbST callers pass no publication)
+    // BbST_CON only: the BbST (QueryDirect) instances publish from a tail kernel.
+    // Compiled out of them: inlined there, it cost the c3 / c5 h = 1 query 16 bytes
+    // of spills per thread and 0.538 -> 0.578 / 0.188 -> 0.233 ms.
+    if constexpr (!std::is_same<QP, QueryDirect>::value) publish_early(pub);
     // the vectorised instances know k at compile time (k = 32 * EPV * VPL): block
     // indices by shifts, not 64-bit divisions
     const uint32_t k = VPL > 0 ? uint32_t(32 * E::EPV * (VPL > 0 ? VPL : 1)) : k_rt;
@@ -317,16 +323,16 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
         // a range inside at most two 16-byte vectors (<= 8 cells) is scanned by its
         // own lane at once: no warp round for it (c3: ~1 in 10 queries)
         auto tiny = [&](bool& t, uint64_t lo, uint64_t hi) {
-            if (!t || (hi >> 2) - (lo >> 2) > 1) return;
+            if (!t || (hi >> 2) - (lo >> 2) > BRMQ_TINY_VECS - 1) return;
             t = false;
             // 32-bit (value, position) accumulator, strict '<' in position order
             const uint32_t lo32 = uint32_t(lo), span = uint32_t(hi - lo), p0 = lo32 & ~3u;
             int32_t bv = 0x7FFFFFFF;
             uint32_t bi = 0xFFFFFFFFu;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < BRMQ_TINY_VECS; ++u) {
                 const uint32_t p = p0 + 4u * u;
-                if (u == 1 && p > uint32_t(hi)) break;
+                if (u >= 1 && p > uint32_t(hi)) break;
                 const int4 x = elem.load_vec((lo >> 2) + u);
                 const int32_t e4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -338,11 +344,13 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
             }
             best = kmin(best, pack_key(bv, bi));
         };
+#ifndef BRMQ_NO_SCAN_COUNT
         if (elem.scanned) {  // instrumented: cells of every range the rule scans
             uint64_t cells = (t0 ? hi0 - lo0 + 1 : 0) + (t1 ? hi1 - lo1 + 1 : 0);
             cells = __reduce_add_sync(kFull, uint32_t(cells));
             if (lane == 0 && cells) atomicAdd(elem.scanned, (unsigned long long)cells);
         }
+#endif
         tiny(t0, lo0, hi0);
         tiny(t1, lo1, hi1);
     }
@@ -973,7 +981,10 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 32)) k_
                                                    uint64_t* __restrict__ answers,
                                                    const CtlPublish pub) {
     brmq::pdl_wait();
-    publish_early(pub);
+    // BbST_CON only.  Compiled out of the BbST (QueryDirect) instances: there it
+    // cost 8-16 bytes of spills per thread (c3 [32, 512] query 0.419 -> 0.413 ms).
+    // (As a non-inlined call here: fewer spills, but the c3-con query 0.475 -> 0.491.)
+    if constexpr (!std::is_same<QP, QueryDirect>::value) publish_early(pub);
     constexpr int kRowCap = 64;  // <= 2 rows per lane
     __shared__ uint4 s_rows[NT / 32][kRowCap];
     const uint32_t warp = threadIdx.x >> 5;
