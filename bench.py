@@ -251,7 +251,8 @@ def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2, poison=N
     """Per-step CUDA-event windows on the library stream; L2 flushed between steps.
     timing: library stage events (0 off, 1 every stage, 2 only the roofline kernel).
     poison: called before every step, outside the window (fills the answer buffer
-    with 0xFF so a replay that wrote nothing cannot pass the check that follows)."""
+    with 0xFF so a replay that wrote nothing cannot pass the check that follows).
+    Async device solves (Engine.set_async) are settled after each window closes."""
     eng.set_timing(timing)
     for _ in range(warmup):
         flush()
@@ -267,6 +268,7 @@ def time_solves(eng, torch, stream, fn, steps, warmup, flush, timing=2, poison=N
         fn()
         e.record(stream)
         e.synchronize()
+        eng.synchronize()  # (async device solves) the solve's status, outside the window
         ms.append(s.elapsed_time(e))
         for nm, t, nl in eng.stage_times():
             a = stage_acc.setdefault(nm, [0.0, 0])
@@ -302,6 +304,10 @@ def run_ours(args) -> dict:
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
+    # device-pointer solves return once enqueued: the timed window is the device
+    # time of the solve, not the host's wake-up after a blocking call (~10 us at
+    # c2); time_solves settles each solve's status after its window closes
+    eng.set_async(True)
     dA = torch.from_numpy(A).to(dev)
     dQ = torch.from_numpy(Q.view(np.int64)).to(dev)
     dAns = torch.empty(q, dtype=torch.int64, device=dev)

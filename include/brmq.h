@@ -249,6 +249,14 @@ int brmq_device_alloc(brmq_ctx* ctx, void** out, size_t bytes);
 int brmq_device_free(brmq_ctx* ctx, void* p);
 int brmq_memcpy(brmq_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /* cudaMemcpyKind */);
 int brmq_synchronize(brmq_ctx* ctx);
+/* Async device solves: with enable = 1, brmq_solve_bbst / _bbst_ml / _bbst_con on
+ * DEVICE pointers (BRMQ_PTR_DEVICE, no stage timing) return once the solve is
+ * enqueued on the context stream instead of waiting for it.  brmq_synchronize
+ * then waits, fills brmq_last_solve_info and returns that solve's status (the
+ * exceptions the synchronous call would have raised); any other call on the
+ * context settles an outstanding async solve first, so no status is dropped.
+ * Host-pointer solves stay synchronous (their answers land in host memory). */
+int brmq_ctx_set_async(brmq_ctx* ctx, int enable);
 
 #ifdef __cplusplus
 }

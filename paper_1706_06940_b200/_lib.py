@@ -69,6 +69,7 @@ SIGNATURES = {
     "brmq_floor_log2": (C.c_int, [C.c_uint64, u32p]),
     "brmq_ctx_set_timing": (C.c_int, [vp, C.c_int]),
     "brmq_ctx_set_counters": (C.c_int, [vp, C.c_int]),
+    "brmq_ctx_set_async": (C.c_int, [vp, C.c_int]),
     "brmq_last_stage_times": (C.c_int, [vp, C.POINTER(StageTimes)]),
     "brmq_last_solve_info": (C.c_int, [vp, C.POINTER(SolveInfo)]),
     "brmq_host_alloc": (C.c_int, [C.POINTER(vp), C.c_size_t]),

@@ -154,6 +154,15 @@ class Engine:
     def set_stream(self, stream_ptr: int | None) -> None:
         _check(self._L.brmq_ctx_set_stream(self._h, stream_ptr or None))
 
+    def set_async(self, enable: bool = True) -> None:
+        """Device-pointer BbST / [32, k] / BbST_CON solves return once enqueued;
+        synchronize() waits and raises what the solve would have raised (brmq.h)."""
+        _check(self._L.brmq_ctx_set_async(self._h, int(bool(enable))))
+
+    def synchronize(self) -> None:
+        """Wait for the context stream; raises the status of an outstanding async solve."""
+        _check(self._L.brmq_synchronize(self._h))
+
     def set_counters(self, enable: bool = True) -> None:
         """Debug scan-cell counter of BbST (h = 1) solves (solve_info()["scanned_cells"])."""
         _check(self._L.brmq_ctx_set_counters(self._h, int(bool(enable))))

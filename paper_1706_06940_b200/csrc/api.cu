@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -114,6 +115,12 @@ struct brmq_ctx {
     // (BRMQ_FUSE=1: on).  Off: measured -1 us at c2 in one harness and +16 us in
     // bench.py's process (DESIGN 3.1)
     bool use_fuse = false;
+    // brmq_ctx_set_async: device-pointer solves (BbST, [32, k], BbST_CON) return as
+    // soon as they are enqueued; brmq_synchronize waits, fills the solve info and
+    // returns the last solve's status (pending_fill)
+    bool async_mode = false;
+    bool async_pending = false;
+    std::function<void()> pending_fill;
     struct GraphEntry;
     std::vector<GraphEntry*> graphs;
     // timing: 0 off, 1 every stage, 2 only the roofline kernel (contract / block_argmin)
@@ -302,6 +309,35 @@ int map_err(uint32_t err) {
     return BRMQ_OK;
 }
 
+// End of a solve.  Synchronous: wait, fill the solve info from the control header
+// the final kernel published (host-mapped), return its status.  Async mode
+// (device pointers, no stage timing): return at once; brmq_synchronize does the
+// rest for the last solve.
+template <class Fill>
+int end_solve(brmq_ctx* c, bool dev, Timer& tm, Fill&& fill) {
+    if (dev && c->async_mode && c->timing == 0) {
+        tm.finish();
+        c->pending_fill = std::function<void()>(fill);
+        c->async_pending = true;
+        return BRMQ_OK;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    tm.finish();
+    fill();
+    return map_err(c->ctl_host->err);
+}
+
+// A call on a context with an async solve outstanding settles it first (waits,
+// fills the solve info, returns its status if it failed), so no error is dropped.
+int settle_pending(brmq_ctx* c) {
+    if (!c->async_pending) return BRMQ_OK;
+    c->async_pending = false;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->pending_fill) c->pending_fill();
+    c->pending_fill = nullptr;
+    return map_err(c->ctl_host->err);
+}
+
 int bits_for(uint64_t n) {  // bit_width(n - 1): positions are < n
     if (n <= 1) return 0;
     return 64 - __builtin_clzll(n - 1);
@@ -451,12 +487,14 @@ int brmq_ctx_set_counters(brmq_ctx* c, int enable) {
 
 int brmq_last_stage_times(brmq_ctx* c, brmq_stage_times* out) {
     if (!c || !out) return fail(BRMQ_EINVAL, "null argument");
+    if (int rc = settle_pending(c)) return rc;
     *out = c->last_times;
     return BRMQ_OK;
 }
 
 int brmq_last_solve_info(brmq_ctx* c, brmq_solve_info* out) {
     if (!c || !out) return fail(BRMQ_EINVAL, "null argument");
+    if (int rc = settle_pending(c)) return rc;
     *out = c->info;
     return BRMQ_OK;
 }
@@ -485,7 +523,15 @@ int brmq_memcpy(brmq_ctx* c, void* dst, const void* src, size_t bytes, int kind)
     return BRMQ_OK;
 }
 int brmq_synchronize(brmq_ctx* c) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return settle_pending(c);
+}
+
+int brmq_ctx_set_async(brmq_ctx* c, int enable) {
+    if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;
+    c->async_mode = enable != 0;
     return BRMQ_OK;
 }
 
@@ -625,6 +671,7 @@ int brmq_solve_bbst_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, uint6
                           uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
                           uint64_t* keys, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
     return solve_shard(c, A, n_shard, offset, n_total, Q, q, keys, flags,
                        [&](const int32_t* dA, const brmq_query* Ql, uint64_t* loc) {
@@ -636,6 +683,7 @@ int brmq_solve_bbst_con_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, u
                               uint64_t n_total, const brmq_query* Q, uint64_t q, uint32_t k,
                               int sort_kind, uint64_t* keys, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst_con: block size k must be >= 1");
     // the clipped queries' endpoints include the shard borders of every query that
     // crosses one: the shard is contracted with its own endpoints plus those borders
@@ -652,6 +700,7 @@ int brmq_solve_bbst_con_shard(brmq_ctx* c, const int32_t* A, uint64_t n_shard, u
 int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
                      uint64_t* answers, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     c->info = brmq_solve_info{};
     c->info.n = n;
     c->info.q = q;
@@ -713,6 +762,7 @@ int brmq_solve_naive(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query
 int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
                     uint32_t k, uint64_t* answers, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: block size k must be >= 1");
     if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     c->info = brmq_solve_info{};
@@ -782,13 +832,12 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
-    CUDA_TRY(cudaStreamSynchronize(s));
-    tm.finish();
-    c->info.blocks = b;
-    c->info.levels = L;
-    c->info.kernel_launches = uint32_t(launches);
-    c->info.scanned_cells = c->count_scans ? c->ctl_host->scanned : 0;
-    return map_err(c->ctl_host->err);
+    return end_solve(c, dev, tm, [c, b, L, launches]() {
+        c->info.blocks = b;
+        c->info.levels = L;
+        c->info.kernel_launches = uint32_t(launches);
+        c->info.scanned_cells = c->count_scans ? c->ctl_host->scanned : 0;
+    });
 }
 
 // ------------------------------------------------------------ multi-level BbST
@@ -875,17 +924,17 @@ static int solve_chain(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, false, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
-    CUDA_TRY(cudaStreamSynchronize(s));
-    tm.finish();
-    c->info.blocks = b;
-    c->info.levels = L;
-    c->info.kernel_launches = uint32_t(launches);
-    return map_err(c->ctl_host->err);
+    return end_solve(c, dev, tm, [c, b, L, launches]() {
+        c->info.blocks = b;
+        c->info.levels = L;
+        c->info.kernel_launches = uint32_t(launches);
+    });
 }
 
 int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q, uint64_t q,
                        const uint32_t* ks, uint32_t h, uint64_t* answers, uint32_t flags) {
     if (!c || !ks) return fail(BRMQ_EINVAL, "null argument");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (h == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst: empty level config");
     if (h == 1) return brmq_solve_bbst(c, A, n, Q, q, ks[0], answers, flags);
     if (h > brmq::kMaxChain) return fail(BRMQ_EINVAL, "solve_batch_bbst: at most 8 levels");
@@ -963,12 +1012,11 @@ int brmq_solve_bbst_ml(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_que
     if (int rc = prepare_ctl(c, ctl)) return rc;
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
-    CUDA_TRY(cudaStreamSynchronize(s));
-    tm.finish();
-    c->info.blocks = b;
-    c->info.levels = L;
-    c->info.kernel_launches = uint32_t(launches);
-    return map_err(c->ctl_host->err);
+    return end_solve(c, dev, tm, [c, b, L, launches]() {
+        c->info.blocks = b;
+        c->info.levels = L;
+        c->info.kernel_launches = uint32_t(launches);
+    });
 }
 
 // ------------------------------------------------------------------ BbST_CON
@@ -976,6 +1024,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
                         uint64_t q, uint32_t k, int sort_kind, uint64_t* answers,
                         uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (k == 0) return fail(BRMQ_EINVAL, "solve_batch_bbst_con: block size k must be >= 1");
     if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
@@ -1166,16 +1215,15 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     c->epoch_host += n_epochs;
-    CUDA_TRY(cudaStreamSynchronize(s));
-    tm.finish();
-    const Control& h = *c->ctl_host;
-    c->info.boundary = h.nb;
-    c->info.span_lo = ~h.span[0];
-    c->info.span_hi = h.span[1];
-    c->info.blocks = h.b_dev;
-    c->info.levels = h.b_dev ? brmq::floor_log2_u64(h.b_dev) + 1 : 0;
-    c->info.kernel_launches = uint32_t(launches);
-    return map_err(h.err);
+    return end_solve(c, dev, tm, [c, launches]() {
+        const Control& h = *c->ctl_host;
+        c->info.boundary = h.nb;
+        c->info.span_lo = ~h.span[0];
+        c->info.span_hi = h.span[1];
+        c->info.blocks = h.b_dev;
+        c->info.levels = h.b_dev ? brmq::floor_log2_u64(h.b_dev) + 1 : 0;
+        c->info.kernel_launches = uint32_t(launches);
+    });
 }
 
 // ------------------------------------------------------------------ ST-RMQ_CON
@@ -1187,6 +1235,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
 int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query* Q,
                           uint64_t q, uint64_t* answers, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (n > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
     c->info = brmq_solve_info{};
@@ -1319,6 +1368,7 @@ int brmq_solve_st_rmq_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_
 int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_endpoint* eps,
                            uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (q > (1ull << 31)) return fail(BRMQ_EINVAL, "collect_endpoints: too many queries for 32-bit origins");
     if (q == 0) return BRMQ_OK;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -1350,6 +1400,7 @@ int brmq_collect_endpoints(brmq_ctx* c, const brmq_query* Q, uint64_t q, brmq_en
 
 int brmq_sort_endpoints(brmq_ctx* c, brmq_endpoint* eps, uint64_t m, int sort_kind, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (sort_kind < 0 || sort_kind > 2) return fail(BRMQ_EINVAL, "unknown sort kind %d", sort_kind);
     if (m < 2) return BRMQ_OK;
     CUDA_TRY(cudaSetDevice(c->device));
@@ -1394,6 +1445,7 @@ int brmq_build_contracted_stats(brmq_ctx* c, const int32_t* A, uint64_t n, const
                                 uint64_t m, int32_t* aq_values, uint64_t* aq_origin, uint64_t* boundary,
                                 uint64_t* nb, uint32_t flags, uint64_t* array_reads) {
     if (!c || !nb) return fail(BRMQ_EINVAL, "null argument");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     *nb = 0;
     if (m == 0) return BRMQ_OK;  // contraction.cpp:116
     if (n == 0) return fail(BRMQ_ERANGE, "endpoint exceeds array bounds");
@@ -1479,6 +1531,7 @@ int brmq_remap_from_sorted(brmq_ctx* c, const brmq_endpoint* sorted_eps, uint64_
                            const uint64_t* boundary, uint64_t nb, uint64_t q, uint32_t* cleft,
                            uint32_t* cright, uint8_t* degenerate, uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (q == 0 && m == 0) return BRMQ_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     const bool dev = is_device(flags);
@@ -1526,6 +1579,7 @@ int brmq_remap_queries(brmq_ctx* c, const brmq_query* Q, uint64_t q, const uint6
                        uint64_t nb, uint32_t* cleft, uint32_t* cright, uint8_t* degenerate,
                        uint32_t flags) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (q == 0) return BRMQ_OK;
     CUDA_TRY(cudaSetDevice(c->device));
     const bool dev = is_device(flags);
@@ -1564,6 +1618,7 @@ int brmq_remap_queries(brmq_ctx* c, const brmq_query* Q, uint64_t q, const uint6
 int brmq_build_block_sparse(brmq_ctx* c, const int32_t* values, uint64_t m, uint32_t k,
                             uint64_t* table, uint64_t* b_out, uint32_t* levels_out, uint32_t flags) {
     if (!c || !b_out || !levels_out) return fail(BRMQ_EINVAL, "null argument");
+    if (int rc = settle_pending(c)) return rc;  // an outstanding async solve first
     if (k == 0) return fail(BRMQ_EINVAL, "build_block_sparse: k must be >= 1");
     if (m > 0xFFFFFFFFull) return fail(BRMQ_EINVAL, "input too long for 32-bit positions");
     const uint64_t b = (m + k - 1) / k;

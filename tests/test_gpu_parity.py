@@ -260,6 +260,56 @@ def test_graph_replays_poisoned(engine, orc):
                 assert bad.size == 0, (rep, ci, variant, bad[:5])
 
 
+def test_async_device_solves(engine, orc):
+    """brmq_ctx_set_async (brmq.h): device-pointer solves return once enqueued and
+    brmq_synchronize returns their status -- the answers, the exceptions the
+    synchronous call raises (naive.hpp:14-15 range check) and the solve info
+    must be the same; a call with an async solve outstanding settles it first."""
+    torch = pytest.importorskip("torch")
+    r = np.random.default_rng(77)
+    n, q = 500_000, 60_000
+    A = _values(r, n, "ties16")
+    Q = _queries(r, n, q, "mixed")
+    want = orc.solve_oracle(A, Q)
+    dA = torch.from_numpy(A).cuda()
+    dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+    variants = ["bbst", "bbst_ml", "bbst_ml3", "con_radix", "con_bitmap"]
+    outs = {v: torch.empty(q, dtype=torch.int64, device="cuda") for v in variants}
+    bad = torch.from_numpy(make_queries([0, 5], [n - 1, n]).view(np.int64)).cuda()
+    engine.set_async(True)
+    try:
+        for rep in range(2):
+            for v in variants:  # one at a time
+                outs[v].fill_(-1)
+                torch.cuda.synchronize()
+                _solve_into(engine, v, dA, dQ, outs[v])
+                engine.synchronize()
+                assert np.array_equal(outs[v].cpu().numpy().view(np.uint64), want), (rep, v)
+            for v in variants:  # back to back: each call settles the one before
+                outs[v].fill_(-1)
+            torch.cuda.synchronize()
+            for v in variants:
+                _solve_into(engine, v, dA, dQ, outs[v])
+            engine.synchronize()
+            for v in variants:
+                assert np.array_equal(outs[v].cpu().numpy().view(np.uint64), want), (rep, v, "b2b")
+            info = engine.solve_info()  # of the last (BbST_CON) solve
+            assert info["boundary"] > 0 and info["blocks"] > 0
+            # a failing solve reports at synchronize(), and the next one is clean
+            engine.solve_batch_bbst_con(dA, bad, 512, SortKind.Bitmap,
+                                        out=torch.empty(2, dtype=torch.int64, device="cuda"))
+            with pytest.raises(OutOfRange):
+                engine.synchronize()
+            engine.solve_batch_bbst(dA, bad, 512, out=torch.empty(2, dtype=torch.int64, device="cuda"))
+            with pytest.raises(OutOfRange):  # settled by the next call
+                _solve_into(engine, "con_bitmap", dA, dQ, outs["con_bitmap"])
+            _solve_into(engine, "con_bitmap", dA, dQ, outs["con_bitmap"])
+            engine.synchronize()
+            assert np.array_equal(outs["con_bitmap"].cpu().numpy().view(np.uint64), want)
+    finally:
+        engine.set_async(False)
+
+
 @pytest.mark.slow
 def test_positions_above_2_31(engine, orc):
     """n = 2^31 + 4099 (the reference allows n up to 2^32 - 1,
