@@ -356,6 +356,10 @@ def run_ours(args) -> dict:
     # per-stage breakdown (every stage bracketed by events; informative, not the headline)
     _, breakdown, _ = time_solves(eng, torch, stream, solve, 5, 1, flush, timing=1, poison=poison)
     checks["stage_pass"] = check("per-stage pass")
+    # preprocess vs query (timing level 3: one event pair around everything before
+    # the query kernel, one around the query -- 4 event nodes instead of 2 per stage)
+    _, phases, _ = time_solves(eng, torch, stream, solve, args.steps, 1, flush, timing=3, poison=poison)
+    checks["phase_pass"] = check("two-phase pass")
     # the other endpoint-sort pipeline on the same workload (same answers)
     variants = {variant: aggregate_value(q, 1, statistics.mean(ms))}
     if variant != "bbst":
@@ -448,7 +452,7 @@ def run_ours(args) -> dict:
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(f"{name}/{variant}/{dom_for_roof}")
-    pre_ms = sum(v[0] for k, v in breakdown.items() if k not in ("query", "h2d", "d2h"))
+    pre_ms = phases.get("preprocess", (float("nan"),))[0]
     pre_bytes = 4 * n if variant == "bbst" else 4 * (info["span_hi"] - info["span_lo"] + 1) + 16 * q + 8 * max(info["boundary"] - 1, 0)
 
     rec = {
@@ -478,7 +482,11 @@ def run_ours(args) -> dict:
                                "K-step pass (step time with those events: "
                                f"{statistics.mean(ms_roof):.4f} ms)"},
         "preprocess": {"ms": pre_ms, "alg_bytes": pre_bytes,
-                       "gbs": pre_bytes / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None},
+                       "gbs": pre_bytes / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None,
+                       "frac": pre_bytes / (pre_ms * 1e-3) / 1e9 / pk["hbm_gbs"] if pre_ms > 0 else None,
+                       "query_ms": phases.get("query", (float("nan"),))[0],
+                       "method": "timing level 3: CUDA events (graph nodes) before the first kernel and "
+                                 "before the query kernel; every kernel of the solve up to the query"},
         "stages_ms": {k: round(v[0], 5) for k, v in breakdown.items()},
         "dominant_stage": dom,
         "variants_queries_per_s": variants,

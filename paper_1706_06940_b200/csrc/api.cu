@@ -247,6 +247,23 @@ struct Timer {
         c->stage_names.emplace_back(name);
         c->stage_launches.push_back(0);
     }
+    // timing level 3: two phases, "preprocess" (everything before the query kernel)
+    // and "query" -- four event nodes per solve instead of two per stage
+    bool ph_open = false;
+    void phase_begin(const char* name) {
+        if (c->timing != 3 || n >= BRMQ_MAX_STAGES) return;
+        record(c->ev[2 * n]);
+        c->stage_names.emplace_back(name);
+        c->stage_launches.push_back(0);
+        ph_open = true;
+    }
+    void phase_end(int launches) {
+        if (!ph_open) return;
+        record(c->ev[2 * n + 1]);
+        c->stage_launches.back() = uint32_t(launches);
+        ++n;
+        ph_open = false;
+    }
     void end(int launches) {
         if (!active || n >= BRMQ_MAX_STAGES) return;
         active = false;
@@ -475,7 +492,7 @@ void* brmq_ctx_stream(brmq_ctx* c) { return c ? static_cast<void*>(c->stream) : 
 
 int brmq_ctx_set_timing(brmq_ctx* c, int enable) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
-    c->timing = enable < 0 ? 0 : (enable > 2 ? 1 : enable);
+    c->timing = enable < 0 ? 0 : (enable > 3 ? 1 : enable);
     return BRMQ_OK;
 }
 
@@ -805,6 +822,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
             CUDA_TRY(c->stager.h2d(const_cast<int32_t*>(dA), A, n * 4, s));
             tm.end(0);
         }
+        tm.phase_begin("preprocess");
         tm.stage("block_argmin", launches);
         l = brmq::launch_block_argmin_i32(dA, n, k, ST, s);
         launches += l;
@@ -813,11 +831,14 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
         l = brmq::launch_sparse_table(ST, b, nullptr, s);
         launches += l;
         tm.end(l);
+        tm.phase_end(launches);
+        tm.phase_begin("query");
         tm.stage("query", launches);
         l = brmq::launch_query_direct(dA, n, k, ST, b, dQ, q, dAns, &ctl->err, s, brmq::CtlPublish{},
                                       c->count_scans ? &ctl->scanned : nullptr);
         launches += l;
         tm.end(l);
+        tm.phase_end(l);
         launches += publish(c, ctl, s);  // control header -> host (k_publish)
         if (int rc = check_status(c)) return rc;
         if (!dev) {
@@ -1117,6 +1138,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         uint64_t* fill0 = fuse ? SUB : nullptr;
         uint64_t* fill1 = fuse ? ST : nullptr;
         const uint64_t fill0_n = fuse ? sub_words : 0, fill1_n = fuse ? b_max : 0;
+        tm.phase_begin("preprocess");
         if (use_bitmap) {
             tm.stage("collect_mark", launches);
             l = brmq::launch_collect(dQ, q, n, nullptr, nullptr, c->bitmap,
@@ -1189,6 +1211,8 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         l = brmq::launch_sparse_table(ST, b_max, &ctl->b_dev, s);
         launches += l;
         tm.end(l);
+        tm.phase_end(launches);
+        tm.phase_begin("query");
         tm.stage("query", launches);
         const uint2* wi = reinterpret_cast<uint2*>(P(i_wi));
         // the query kernel writes nothing into the control header: its first warp
@@ -1201,6 +1225,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
                                                  publish_ctl(c, ctl));
         launches += l;
         tm.end(l);
+        tm.phase_end(l);
         if (int rc = check_status(c)) return rc;
         if (!dev) {
             tm.stage("d2h", launches);
