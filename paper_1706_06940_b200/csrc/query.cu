@@ -49,16 +49,18 @@ constexpr int kThreads = 256;
 #ifndef BRMQ_FLAT_WARPS
 #define BRMQ_FLAT_WARPS 56
 #endif
-#ifndef BRMQ_TINY_VECS
-#define BRMQ_TINY_VECS 2  // ranges within this many 16-byte vectors: scanned lane-private
-#endif
 #ifndef BRMQ_QUERY_WARPS
 #define BRMQ_QUERY_WARPS 48
 #endif
 
-struct ElemI32 {
+// WHOLE: len is a multiple of 4, so every vector a scan touches lies inside the
+// array and load_vec is one unchecked 128-bit load (c3: the per-vector tail test
+// was ~8% of the h = 1 query kernel's instructions).
+template <bool WHOLE>
+struct ElemI32T {
     using vec_t = int4;
     static constexpr int EPV = 4;
+    static constexpr bool kI32 = true;
     const int32_t* data;
     uint64_t len;
     unsigned long long* scanned = nullptr;  // debug counter (launch_query_direct)
@@ -68,7 +70,7 @@ struct ElemI32 {
     // 128-bit load when the vector lies inside the array, scalar tail otherwise
     // (never touches memory past `len`; out-of-range lanes are masked later).
     __device__ __forceinline__ vec_t load_vec(uint64_t v) const {
-        if (v * 4 + 3 < len) return ld_stream_v4(reinterpret_cast<const int4*>(data) + v);
+        if (WHOLE || v * 4 + 3 < len) return ld_stream_v4(reinterpret_cast<const int4*>(data) + v);
         int4 x = make_int4(0, 0, 0, 0);
         if (v * 4 + 0 < len) x.x = __ldg(data + v * 4 + 0);
         if (v * 4 + 1 < len) x.y = __ldg(data + v * 4 + 1);
@@ -94,10 +96,12 @@ struct ElemI32 {
         __device__ __forceinline__ uint64_t key() const { return bi == 0xFFFFFFFFu ? kNoKey : pack_key(bv, bi); }
     };
 };
+using ElemI32 = ElemI32T<false>;
 
 struct ElemKey {
     using vec_t = uint4;
     static constexpr int EPV = 2;
+    static constexpr bool kI32 = false;
     const uint64_t* data;  // allocation padded to a multiple of 2 keys by the caller
     __device__ __forceinline__ uint64_t key_at(uint64_t i) const { return __ldg(data + i); }
     __device__ __forceinline__ vec_t load_vec(uint64_t v) const {
@@ -218,8 +222,8 @@ __device__ __forceinline__ uint32_t vec_first_eq(const int4& x, uint32_t a, uint
 // ~30 instructions per lane for a range of <= 32 vectors (NJ = 1), against ~90
 // for the per-element (value, position) accumulator it replaces (ncu: the c3
 // h = 1 query kernel was issue-bound, 69% of issue slots busy).
-template <int NJ>
-__device__ __forceinline__ uint64_t scan_i32_vecs(const ElemI32& e, uint64_t v0, uint32_t nv,
+template <int NJ, class E>
+__device__ __forceinline__ uint64_t scan_i32_vecs(const E& e, uint64_t v0, uint32_t nv,
                                                   uint32_t lo_t, uint32_t hi_t) {
     const uint32_t lane = lane_id();
     int4 x[NJ];
@@ -251,12 +255,12 @@ __device__ __forceinline__ uint64_t scan_i32_vecs(const ElemI32& e, uint64_t v0,
     return pack_key(wv, uint32_t(4 * v0) + off);
 }
 
-template <int VPL>
-__device__ __forceinline__ uint64_t scan_i32(const ElemI32& e, uint32_t lo, uint32_t hi) {
+template <int VPL, class E>
+__device__ __forceinline__ uint64_t scan_i32(const E& e, uint32_t lo, uint32_t hi) {
     const uint64_t v0 = lo >> 2;
     const uint32_t nv = (hi >> 2) - (lo >> 2) + 1u;
-    if (VPL <= 1 || nv <= 32u) return scan_i32_vecs<1>(e, v0, nv, lo & 3u, hi & 3u);
-    return scan_i32_vecs<(VPL > 1 ? VPL : 1)>(e, v0, nv, lo & 3u, hi & 3u);
+    if (VPL <= 1 || nv <= 32u) return scan_i32_vecs<1, E>(e, v0, nv, lo & 3u, hi & 3u);
+    return scan_i32_vecs<(VPL > 1 ? VPL : 1), E>(e, v0, nv, lo & 3u, hi & 3u);
 }
 
 template <class E>
@@ -319,30 +323,25 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
         }
     }
 
-    if constexpr (std::is_same<E, ElemI32>::value && VPL > 0) {
+    if constexpr (E::kI32 && VPL > 0) {
         // a range inside at most two 16-byte vectors (<= 8 cells) is scanned by its
         // own lane at once: no warp round for it (c3: ~1 in 10 queries)
         auto tiny = [&](bool& t, uint64_t lo, uint64_t hi) {
-            if (!t || (hi >> 2) - (lo >> 2) > BRMQ_TINY_VECS - 1) return;
+            if (!t || (hi >> 2) - (lo >> 2) > 1) return;
             t = false;
-            // 32-bit (value, position) accumulator, strict '<' in position order
-            const uint32_t lo32 = uint32_t(lo), span = uint32_t(hi - lo), p0 = lo32 & ~3u;
-            int32_t bv = 0x7FFFFFFF;
-            uint32_t bi = 0xFFFFFFFFu;
-#pragma unroll
-            for (int u = 0; u < BRMQ_TINY_VECS; ++u) {
-                const uint32_t p = p0 + 4u * u;
-                if (u >= 1 && p > uint32_t(hi)) break;
-                const int4 x = elem.load_vec((lo >> 2) + u);
-                const int32_t e4[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int t2 = 0; t2 < 4; ++t2)
-                    if (p + t2 - lo32 <= span && (e4[t2] < bv || bi == 0xFFFFFFFFu)) {
-                        bv = e4[t2];
-                        bi = p + t2;
-                    }
-            }
-            best = kmin(best, pack_key(bv, bi));
+            // masked 3-way minima of the one or two vectors, then the first element
+            // equal to the minimum (leftmost: the first vector wins ties)
+            const uint32_t lo32 = uint32_t(lo), hi32 = uint32_t(hi);
+            const bool two = (hi32 >> 2) != (lo32 >> 2);
+            const int4 x0 = elem.load_vec(lo >> 2);
+            const int4 x1 = two ? elem.load_vec((lo >> 2) + 1) : x0;
+            const uint32_t a0 = lo32 & 3u, b0 = two ? 3u : (hi32 & 3u), b1 = hi32 & 3u;
+            const int32_t m0 = vec_min_masked(x0, a0, b0);
+            const int32_t m1 = two ? vec_min_masked(x1, 0u, b1) : 0x7FFFFFFF;
+            const int32_t wv = min(m0, m1);
+            const uint32_t pos = m0 == wv ? (lo32 & ~3u) + vec_first_eq(x0, a0, b0, wv)
+                                          : (lo32 & ~3u) + 4u + vec_first_eq(x1, 0u, b1, wv);
+            best = kmin(best, pack_key(wv, pos));
         };
 #ifndef BRMQ_NO_SCAN_COUNT
         if (elem.scanned) {  // instrumented: cells of every range the rule scans
@@ -356,7 +355,7 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
     }
     // Warp-cooperative partial-block scans.
     unsigned m0 = __ballot_sync(kFull, t0), m1 = __ballot_sync(kFull, t1);
-    if constexpr (std::is_same<E, ElemI32>::value && VPL > 0) {
+    if constexpr (E::kI32 && VPL > 0) {
         // int32 A (BbST): ranges prefetched into L2 at once, then one range per
         // round by the value-then-position scan (positions < 2^32: 32-bit shuffles)
         // (whole vectors inside the array only: the last partial vector is not prefetched)
@@ -417,7 +416,7 @@ __device__ __forceinline__ void query_body(E elem, QP qp, uint32_t k_rt,
                 lo = __shfl_sync(kFull, uint32_t(lo1), sl);
                 hi = __shfl_sync(kFull, uint32_t(hi1), sl);
             }
-            const uint64_t kb = scan_i32<VPL>(elem, lo, hi);
+            const uint64_t kb = scan_i32<VPL, E>(elem, lo, hi);
             if (int(lane) == sl) best = kmin(best, kb);
         }
         m0 = m1 = 0;
@@ -527,7 +526,12 @@ void dispatch_i32(ElemI32 e, QP qp, uint32_t k, const uint64_t* ST, uint64_t str
     const bool aligned = (reinterpret_cast<uintptr_t>(e.data) & 15u) == 0 && e.len <= 0xFFFFFFFFull - 4096;
     // one pending range per round: fewer registers -> more resident warps, which
     // beats batching ranges per round on this latency-bound kernel (measured)
-    if (aligned && k == 512) return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    if (aligned && k == 512) {
+        if ((e.len & 3u) == 0)  // whole vectors: no tail test per load (ElemI32T)
+            return launch_q<ElemI32T<true>, QP, 4, 1>(ElemI32T<true>{e.data, e.len, e.scanned}, qp, k, ST, stride,
+                                                        q, ans, s, pub);
+        return launch_q<ElemI32, QP, 4, 1>(e, qp, k, ST, stride, q, ans, s, pub);
+    }
     if (aligned && k == 256) return launch_q<ElemI32, QP, 2, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (aligned && k == 1024) return launch_q<ElemI32, QP, 8, 1>(e, qp, k, ST, stride, q, ans, s, pub);
     if (aligned && k == 2048) return launch_q<ElemI32, QP, 16, 1>(e, qp, k, ST, stride, q, ans, s, pub);
