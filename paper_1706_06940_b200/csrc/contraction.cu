@@ -66,7 +66,17 @@ static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
 #ifndef BRMQ_CONTRACT_MINB
 #define BRMQ_CONTRACT_MINB 2  // 2 CTAs per SM: <= 128 registers (129 would halve the residency)
 #endif
-constexpr int kDense = BRMQ_KDENSE;  // flagged rows per warp tile above which rows close per lane
+constexpr int kDense = BRMQ_KDENSE;
+#ifdef BRMQ_CONTRACT_STAMPS
+// A/B diagnostics: per warp (start, loop end, stitch end) %globaltimer stamps of the
+// last contraction launch (tools/contract_tail.py)
+__device__ unsigned long long g_cstamp[kMaxContractRanges * 8][3];
+__device__ __forceinline__ unsigned long long cgt() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif  // flagged rows per warp tile above which rows close per lane
 constexpr int kDenseEndpoints = 8;  // endpoints per warp tile from which only dense rows are compiled in
 
 // Rows of the current warp tile in the warp's swizzled shared rows (16-byte
@@ -719,6 +729,10 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         const uint64_t hi = (wa + cnt) * kWTile - 1 < blast ? (wa + cnt) * kWTile - 1 : blast;
         if (hi >= lo) atomicAdd(reinterpret_cast<unsigned long long*>(c.reads), (unsigned long long)(hi - lo + 1));
     }
+#ifdef BRMQ_CONTRACT_STAMPS
+    const uint64_t gw_dbg = uint64_t(blockIdx.x) * NW + warp;
+    if (lane == 0) g_cstamp[gw_dbg][0] = cgt();
+#endif
     if (cnt) stage();
     for (uint64_t i = 0; i < cnt; ++i) {
         const uint32_t fl = fy;
@@ -731,6 +745,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         if (i + 1 < cnt) stage();
     }
 
+#ifdef BRMQ_CONTRACT_STAMPS
+    if (lane == 0) g_cstamp[gw_dbg][1] = cgt();
+#endif
     // ---- stitch: the area closed by each piece's first boundary
     const unsigned hl = __ballot_sync(kFull, head_set);
     if (hl) head = __shfl_sync(kFull, head, __ffs(hl) - 1);
@@ -747,6 +764,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         c.key_tail[cta] = x.k;
         st_release_u64(c.st_part + cta, status_pack(epoch, kStInclusive, x.f != 0, 0));
     }
+#ifdef BRMQ_CONTRACT_STAMPS
+    if (lane == 0 && (!carry.f || rank_first == 0)) g_cstamp[gw_dbg][2] = cgt();
+#endif
     if (!carry.f || rank_first == 0) return;  // no boundary, or the global first one
     // fold the tails of the earlier pieces of this CTA back to one holding a boundary
     uint64_t acc = kNoKey;
@@ -780,6 +800,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         }
     }
     if (lane == 0) put_area<MARKED, FUSE>(out, rank_first - 1, kmin(acc, s_head[warp]));
+#ifdef BRMQ_CONTRACT_STAMPS
+    if (lane == 0) g_cstamp[gw_dbg][2] = cgt();
+#endif
 }
 
 template <bool VEC, bool MARKED, bool SPARSE = true, bool FUSE = false>
@@ -820,6 +843,15 @@ int contract_grid() {
 }
 
 }  // namespace
+
+#ifdef BRMQ_CONTRACT_STAMPS
+extern "C" int brmq_debug_contract_stamps(unsigned long long* out, int n) {
+    const int rc = int(cudaMemcpyFromSymbol(out, g_cstamp, size_t(n) * 3 * 8));
+    static unsigned long long zero[kMaxContractRanges * 8][3];
+    cudaMemcpyToSymbol(g_cstamp, zero, sizeof(zero));
+    return rc;
+}
+#endif
 
 size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
 size_t contract_bitmap_words(uint64_t n) { return contract_tiles(n) * (kTile / 32) + 4; }

@@ -44,7 +44,7 @@ def test_stack_budget():
 
 def test_hot_instances_spill_free():
     usage = {n: (r, s) for n, r, s in _usage()}
-    hot = ["k_query_budgetINS0_7ElemI32ENS0_11QueryDirectELi4ELi1E", "k_contract", "k_msd_partition",
+    hot = ["k_query_budgetINS0_8ElemI32T", "k_contract", "k_msd_partition",
            "k_bucket_mark", "k_block_argmin_i32_vec", "k_st_tile", "k_collect"]
     for h in hot:
         hits = [(n, rs) for n, rs in usage.items() if h in n]

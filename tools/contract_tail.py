@@ -1,0 +1,60 @@
+"""Contraction tail diagnostics (A/B build with -DBRMQ_CONTRACT_STAMPS): per-warp
+start / loop-end / stitch-end %globaltimer stamps of one c2 solve.
+
+    BRMQ_LIB=ab/stamps.so python tools/contract_tail.py [--config c2] [--variant con_bitmap]
+"""
+import argparse, ctypes as C, sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from bench import gen_workload, VARIANT_SORT, L2Flush  # noqa: E402
+from paper_1706_06940_b200 import Engine, _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument('--config', default='c2')
+ap.add_argument('--variant', default='con_bitmap')
+a = ap.parse_args()
+A, Q = gen_workload(a.config)
+eng = Engine(0)
+dA = torch.from_numpy(A).cuda()
+dQ = torch.from_numpy(Q.view(np.int64)).cuda()
+L = _lib.lib()
+f = L.brmq_debug_contract_stamps
+f.argtypes = [C.c_void_p, C.c_int]
+W = 2048 * 8
+buf = np.zeros((W, 3), np.uint64)
+flush = L2Flush(torch, 'cuda')
+for it in range(4):
+    flush()
+    torch.cuda.synchronize()
+    eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[a.variant])
+    torch.cuda.synchronize()
+    f(buf.ctypes.data, W)
+live = buf[(buf[:, 0] > 0) & (buf[:, 1] > 0)]
+t0 = live[:, 0].min()
+s, e1, e2 = (live[:, 0] - t0) / 1e3, (live[:, 1] - t0) / 1e3, (live[:, 2] - t0) / 1e3
+print(f"warps {len(live)}; start: min 0 max {s.max():.2f} us; loop end: min {e1.min():.2f} "
+      f"p10 {np.percentile(e1, 10):.2f} p50 {np.median(e1):.2f} p90 {np.percentile(e1, 90):.2f} max {e1.max():.2f}; "
+      f"stitch end max {e2.max():.2f}")
+# lost warp-time: sum over warps of (kernel end - loop end) / (warps * kernel span)
+span = e2.max()
+print(f"idle fraction after the loop: {np.mean(span - e1) / span:.3f}; mean loop time {np.mean(e1 - s):.2f} us")
+hist, edges = np.histogram(e1, bins=12)
+print("loop-end histogram:", " ".join(f"{edges[i]:.0f}:{hist[i]}" for i in range(len(hist))))
+# within-CTA vs across-CTA spread (8 warps per CTA)
+ends = {}
+for w in range(W):
+    if buf[w, 0] > 0 and buf[w, 1] > 0:
+        ends.setdefault(w // 8, []).append((buf[w, 1] - t0) / 1e3)
+cta_max = np.array([max(v) for v in ends.values() if len(v) == 8])
+cta_min = np.array([min(v) for v in ends.values() if len(v) == 8])
+cta_mean = np.array([np.mean(v) for v in ends.values() if len(v) == 8])
+print(f"CTAs {len(cta_max)}: within-CTA spread (max-min) mean {np.mean(cta_max - cta_min):.2f} us p90 "
+      f"{np.percentile(cta_max - cta_min, 90):.2f}; CTA mean loop end p10 {np.percentile(cta_mean, 10):.2f} "
+      f"p50 {np.median(cta_mean):.2f} p90 {np.percentile(cta_mean, 90):.2f} max {cta_mean.max():.2f}")
+# SM pairing: CTAs b and b + 148 likely share an SM? print correlation of neighbours
+st_minus_loop = (live[:, 2] - live[:, 1]) / 1e3
+print(f"stitch time per warp: p50 {np.median(st_minus_loop):.2f} p90 {np.percentile(st_minus_loop, 90):.2f} max {st_minus_loop.max():.2f}")
+late = np.argsort(-(buf[:, 2].astype(np.int64) - int(t0)))[:5]
+for w in late:
+    print(f"  warp {w} (cta {w // 8}): start {(buf[w,0]-t0)/1e3:.2f} loop end {(buf[w,1]-t0)/1e3:.2f} stitch end {(buf[w,2]-t0)/1e3:.2f}")
