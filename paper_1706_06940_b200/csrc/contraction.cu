@@ -391,8 +391,8 @@ struct ContractArgs {
     const uint32_t* rcnt;  // [G] boundaries per range, or (prefix) [G+1] exclusive prefix
     uint64_t range_tiles;  // R
     uint32_t prefix;
-    uint64_t* st_part;   // [G] epoch-tagged partial descriptors
-    uint64_t* key_tail;  // [G]
+    uint64_t* st_part;   // [G * NW] epoch-tagged descriptors, one per piece
+    uint64_t* key_tail;  // [G * NW]
     const uint32_t* pcnt;  // nullable: [G * NW] boundaries per piece (k_piece_count)
     const uint32_t* epoch_dev;  // device epoch counter (bumped once per solve)
     uint32_t epoch_off;
@@ -420,9 +420,6 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     __shared__ __align__(128) int4 s_rows[NW][kWTile / 4];  // per warp: 32 rows x 128 B, swizzled
     extern __shared__ __align__(16) uint2 s_cap[];  // [NW][kCap][32] boundary captures (dense rows)
     __shared__ uint32_t s_cnt[NW];
-    __shared__ uint64_t s_tail[NW];
-    __shared__ uint32_t s_has[NW];
-    __shared__ uint64_t s_head[NW];  // partial of the area closed by the piece's first boundary
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_red[NW];
 
@@ -748,58 +745,50 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
 #ifdef BRMQ_CONTRACT_STAMPS
     if (lane == 0) g_cstamp[gw_dbg][1] = cgt();
 #endif
-    // ---- stitch: the area closed by each piece's first boundary
+    // ---- stitch: every warp publishes its piece's descriptor (the open segment at
+    // its end, has-boundary) at once -- no block barrier, so a warp never waits
+    // for the slowest warp of its CTA (c2: 7 us apart on average) -- and the area
+    // closed by its first boundary folds the tails of the pieces before it back to
+    // the nearest one holding a boundary (usually the previous warp's).
     const unsigned hl = __ballot_sync(kFull, head_set);
     if (hl) head = __shfl_sync(kFull, head, __ffs(hl) - 1);
+    const int64_t gw = int64_t(cta) * NW + warp;
     if (lane == 0) {
-        s_tail[warp] = carry.k;
-        s_has[warp] = carry.f;
-        s_head[warp] = head;
-    }
-    __syncthreads();
-    if (warp == 0 && lane == 0) {  // the CTA's descriptor: its pieces folded in order
-        SegMin x{kNoKey, 0};
-#pragma unroll
-        for (int w = 0; w < NW; ++w) x = seg_combine(x, SegMin{s_tail[w], s_has[w]});
-        c.key_tail[cta] = x.k;
-        st_release_u64(c.st_part + cta, status_pack(epoch, kStInclusive, x.f != 0, 0));
+        c.key_tail[gw] = carry.k;
+        st_release_u64(c.st_part + gw, status_pack(epoch, kStInclusive, carry.f != 0, 0));
     }
 #ifdef BRMQ_CONTRACT_STAMPS
     if (lane == 0 && (!carry.f || rank_first == 0)) g_cstamp[gw_dbg][2] = cgt();
 #endif
     if (!carry.f || rank_first == 0) return;  // no boundary, or the global first one
-    // fold the tails of the earlier pieces of this CTA back to one holding a boundary
     uint64_t acc = kNoKey;
-    bool found = false;
-    for (int w = int(warp) - 1; w >= 0 && !found; --w) {
-        acc = kmin(acc, s_tail[w]);
-        found = s_has[w] != 0;
-    }
-    if (!found && ta != tfirst) {  // ... and across CTAs
-        int64_t p = int64_t(cta) - 1;
-        bool done = false;
-        while (!done) {
-            const int64_t j = p - int64_t(lane);
-            uint64_t sw = 0, k = kNoKey;
-            bool has = false;
-            const bool live = j >= int64_t(cfirst);  // CTAs before b0's hold nothing
-            if (live) {
-                // backoff: a spinning warp would take issue slots from the warps of
-                // its SM still streaming (c5-con: 4.1M polls per solve without it)
-                while (status_state(sw = ld_relaxed_u64(c.st_part + j), epoch) == kStInvalid)
-                    __nanosleep(256);
-                has = status_flag(sw);
+    const int64_t wfirst = int64_t(cfirst) * NW;  // pieces before b0's CTA hold nothing
+    for (int64_t p = gw - 1; p >= wfirst; p -= 32) {
+        const int64_t j = p - int64_t(lane);
+        const bool live = j >= wfirst;
+        uint64_t sw = 0;
+        bool ready = !live, has = false;
+        while (true) {  // wait only for the descriptors up to the nearest boundary
+            if (!ready) {
+                sw = ld_relaxed_u64(c.st_part + j);
+                ready = status_state(sw, epoch) != kStInvalid;
+                has = ready && status_flag(sw);
             }
-            __threadfence();  // acquire: the tails were stored before their descriptors
-            if (live) k = ld_relaxed_u64(c.key_tail + j);
-            const unsigned hm = __ballot_sync(kFull, has || !live);
-            const int g = hm ? __ffs(hm) - 1 : 32;
-            acc = kmin(acc, warp_min_key(int(lane) <= g ? k : kNoKey));
-            done = g < 32;
-            p -= 32;
+            const unsigned stop = __ballot_sync(kFull, has || !live);
+            const int g = stop ? __ffs(stop) - 1 : 31;
+            const unsigned need = g >= 31 ? kFull : ((2u << g) - 1u);
+            if ((__ballot_sync(kFull, ready) & need) == need) break;
+            // backoff: a spinning warp takes issue slots from the streaming warps
+            __nanosleep(64);
         }
+        __threadfence();  // acquire: the tails were stored before their descriptors
+        const unsigned stop = __ballot_sync(kFull, has || !live);
+        const int g = stop ? __ffs(stop) - 1 : 32;
+        const uint64_t k = (live && int(lane) <= g) ? ld_relaxed_u64(c.key_tail + j) : kNoKey;
+        acc = kmin(acc, warp_min_key(k));
+        if (g < 32) break;
     }
-    if (lane == 0) put_area<MARKED, FUSE>(out, rank_first - 1, kmin(acc, s_head[warp]));
+    if (lane == 0) put_area<MARKED, FUSE>(out, rank_first - 1, kmin(acc, head));
 #ifdef BRMQ_CONTRACT_STAMPS
     if (lane == 0) g_cstamp[gw_dbg][2] = cgt();
 #endif
@@ -855,7 +844,7 @@ extern "C" int brmq_debug_contract_stamps(unsigned long long* out, int n) {
 
 size_t contract_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
 size_t contract_bitmap_words(uint64_t n) { return contract_tiles(n) * (kTile / 32) + 4; }
-size_t contract_status_words() { return size_t(2) * kMaxContractRanges; }  // st_part, key_tail
+size_t contract_status_words() { return size_t(2) * kMaxContractRanges * NW; }  // st_part, key_tail (per piece)
 
 int launch_piece_count(const uint32_t* bitmap, const uint32_t* span, uint64_t n, uint32_t* pcnt,
                        uint32_t* rcnt, cudaStream_t s) {
@@ -890,7 +879,7 @@ int launch_contract(const int32_t* A, uint64_t n, uint32_t* bitmap, const uint32
     // the table's row 0 with kNoKey)
     const bool fz = fuse && vec && !marked;
     ContractArgs args{A, n, bitmap, span, aq, nb_out, aq_len, word_info, rcnt, R,
-                      prefix ? 1u : 0u, status, status + kMaxContractRanges, pcnt, epoch_dev,
+                      prefix ? 1u : 0u, status, status + size_t(kMaxContractRanges) * NW, pcnt, epoch_dev,
                       epoch_off, fz ? fuse->sub : nullptr, fz ? fuse->st : nullptr,
                       fz ? fuse->b_max : 0, fz ? fuse->kshift : 0u, fz ? fuse->b_dev : nullptr,
                       array_reads};

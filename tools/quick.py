@@ -27,6 +27,7 @@ ap.add_argument('--q', type=int, default=None)
 a = ap.parse_args()
 
 eng = Engine(0)
+eng.set_async(True)  # as bench.py: the window is the device time of the solve
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 eng.set_stream(s.cuda_stream)
