@@ -115,6 +115,9 @@ struct brmq_ctx {
     // (BRMQ_FUSE=1: on).  Off: measured -1 us at c2 in one harness and +16 us in
     // bench.py's process (DESIGN 3.1)
     bool use_fuse = false;
+    // BbST_CON: the contraction and the query kernel as PDL secondaries of their
+    // predecessors, each issuing its independent loads before its wait (BRMQ_PDL_QUERY=0: off)
+    bool pdl_query = true;
     // brmq_ctx_set_async: device-pointer solves (BbST, [32, k], BbST_CON) return as
     // soon as they are enqueued; brmq_synchronize waits, fills the solve info and
     // returns the last solve's status (pending_fill)
@@ -462,6 +465,7 @@ int brmq_ctx_create(brmq_ctx** out, int device) {
     if (const char* g = getenv("BRMQ_PDL")) c->use_pdl = atoi(g) != 0;
     if (const char* g = getenv("BRMQ_FUSE")) c->use_fuse = atoi(g) != 0;
     if (const char* g = getenv("BRMQ_MSD")) c->use_msd = atoi(g) != 0;
+    if (const char* g = getenv("BRMQ_PDL_QUERY")) c->pdl_query = atoi(g) != 0;
     *out = c;
     return BRMQ_OK;
 }
@@ -1192,10 +1196,15 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         tm.stage("contract", launches);
         const brmq::ContractFuse fz{SUB, ST, b_max, brmq::floor_log2_u64(k), &ctl->b_dev};
         bool fused = false;
+        // a PDL secondary of the piece count: its first tile loads are issued
+        // before its griddepcontrol.wait (contraction.cu contract_body)
+        const brmq::PdlState pdl_before = brmq::pdl_state();
+        if (c->timing == 0 && c->pdl_query) brmq::pdl_state() = brmq::PdlState{true, false};
         l = brmq::launch_contract(dA, n, c->bitmap, ctl->span, ctl->rcnt, false, AQ,
                                   &ctl->nb, &ctl->aq_len, reinterpret_cast<uint2*>(P(i_wi)), cst,
                                   c->epoch_dev, 0, s, false, pcnt, 2 * q,
                                   fuse ? &fz : nullptr, &fused);
+        brmq::pdl_state() = pdl_before;
         launches += l;
         tm.end(l);
         // (bitmap pipeline: the query remap is folded into the query kernel)
@@ -1217,12 +1226,17 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
         const uint2* wi = reinterpret_cast<uint2*>(P(i_wi));
         // the query kernel writes nothing into the control header: its first warp
         // publishes it (publish_early), no k_publish launch
+        // the query kernel as a PDL secondary of the table build: it resolves its
+        // queries (Q + word info) before its griddepcontrol.wait (query.cu k_query_flat)
+        const brmq::PdlState pdl_saved = brmq::pdl_state();
+        if (c->timing == 0 && c->pdl_query && sub_level) brmq::pdl_state() = brmq::PdlState{true, false};
         if (sub_level)
             l = brmq::launch_query_con_flat(AQ, k, ST, b_max, SUB, dQ, wi, nullptr, nullptr, n, q, dAns, s,
                                             publish_ctl(c, ctl));
         else
             l = brmq::launch_query_contracted_wi(AQ, k, ST, b_max, dQ, wi, n, q, dAns, s,
                                                  publish_ctl(c, ctl));
+        brmq::pdl_state() = pdl_saved;
         launches += l;
         tm.end(l);
         tm.phase_end(l);

@@ -482,6 +482,11 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         if (MARKED) __syncwarp();
     };
     if (cnt) fetch(0);
+    // A PDL secondary of the piece count (BbST_CON) waits here: the span, the epoch
+    // and the bitmap come from the endpoint kernel before it (complete when this
+    // grid was scheduled), so the first tile of A is already in flight; the
+    // per-piece / per-range counts below are the predecessor's (a no-op otherwise)
+    brmq::pdl_wait();
 
     // ---- rank bases: the CTA's from the endpoint stage's per-range counts, the
     // warp's from a popcount of its piece of the bitmap (loads overlap the ring)
@@ -796,9 +801,8 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
 
 template <bool VEC, bool MARKED, bool SPARSE = true, bool FUSE = false>
 __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
-    brmq::pdl_wait();
     brmq::pdl_trigger();  // small grid: dependents may be scheduled now
-    contract_body<VEC, MARKED, SPARSE, FUSE>(c);
+    contract_body<VEC, MARKED, SPARSE, FUSE>(c);  // (its griddepcontrol.wait follows the first loads)
 }
 
 int contract_grid() {

@@ -869,12 +869,13 @@ __device__ __forceinline__ uint64_t side_flat(const uint64_t* __restrict__ sub, 
 // One warp answers queries [g * 32, g * 32 + 32) (lane = query).  E: row loader
 // of the scanned array (A, or A_Q), QP: query resolution (direct, or the
 // contracted coordinates of BbST_CON).
+// `pre`: the lane's query already resolved by the caller (before its PDL wait).
 template <class E, class QP>
 __device__ __forceinline__ void ml_flat_group(const E& elem, const QP& qp, uint32_t kshift,
                                               const uint64_t* __restrict__ ST, uint64_t stride,
                                               const uint64_t* __restrict__ sub, uint64_t q,
                                               uint64_t* __restrict__ answers, uint64_t g,
-                                              uint4* s_rows) {
+                                              uint4* s_rows, const Resolved* pre = nullptr) {
     const uint32_t lane = lane_id();
     const bool upper = lane >= 16;
     const uint32_t j = lane & 15u;
@@ -889,7 +890,7 @@ __device__ __forceinline__ void ml_flat_group(const E& elem, const QP& qp, uint3
     if (i < q) {
         // queries, answers and the rows are streamed (evict-first): the Sparse
         // Table and the sub-block keys stay in L2 (measured: -7% on c3)
-        const Resolved rq = qp.resolve(i);
+        const Resolved rq = pre ? *pre : qp.resolve(i);
         if (rq.done) {
             __stcs(reinterpret_cast<unsigned long long*>(answers + i), (unsigned long long)rq.direct);
         } else {
@@ -984,16 +985,29 @@ __global__ void __launch_bounds__(NT, (NT == 128 ? BRMQ_FLAT_WARPS / 4 : 32)) k_
                                                    const uint64_t* __restrict__ sub, uint64_t q,
                                                    uint64_t* __restrict__ answers,
                                                    const CtlPublish pub) {
-    brmq::pdl_wait();
-    // BbST_CON only.  Compiled out of the BbST (QueryDirect) instances: there it
-    // cost 8-16 bytes of spills per thread (c3 [32, 512] query 0.419 -> 0.413 ms).
-    // (As a non-inlined call here: fewer spills, but the c3-con query 0.475 -> 0.491.)
-    if constexpr (!std::is_same<QP, QueryDirect>::value) publish_early(pub);
     constexpr int kRowCap = 64;  // <= 2 rows per lane
     __shared__ uint4 s_rows[NT / 32][kRowCap];
     const uint32_t warp = threadIdx.x >> 5;
     const uint64_t g = uint64_t(blockIdx.x) * (NT / 32) + warp;
-    if (g < (q + 31) / 32) ml_flat_group(elem, qp, kshift, ST, stride, sub, q, answers, g, s_rows[warp]);
+    if constexpr (std::is_same<QP, QueryContractedWI>::value && NT == 32) {
+        // BbST_CON (bitmap pipeline) small batches (one wave of 1-warp CTAs), a PDL secondary of the Sparse Table build:
+        // the query and its contracted coordinates (the contraction's word info,
+        // complete before the table build began) are read before the wait, while
+        // the table's upper rows are still being written
+        const uint64_t i = g * 32 + lane_id();
+        Resolved rq{};
+        if (i < q) rq = qp.resolve(i);
+        brmq::pdl_wait();
+        publish_early(pub);
+        if (g < (q + 31) / 32) ml_flat_group(elem, qp, kshift, ST, stride, sub, q, answers, g, s_rows[warp], &rq);
+    } else {
+        brmq::pdl_wait();
+        // BbST_CON only.  Compiled out of the BbST (QueryDirect) instances: there it
+        // cost 8-16 bytes of spills per thread (c3 [32, 512] query 0.419 -> 0.413 ms).
+        // (As a non-inlined call here: fewer spills, but the c3-con query 0.475 -> 0.491.)
+        if constexpr (!std::is_same<QP, QueryDirect>::value) publish_early(pub);
+        if (g < (q + 31) / 32) ml_flat_group(elem, qp, kshift, ST, stride, sub, q, answers, g, s_rows[warp]);
+    }
 }
 
 // 128-thread CTAs for large batches: a CTA holds its slot until its slowest

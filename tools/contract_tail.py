@@ -58,3 +58,31 @@ print(f"stitch time per warp: p50 {np.median(st_minus_loop):.2f} p90 {np.percent
 late = np.argsort(-(buf[:, 2].astype(np.int64) - int(t0)))[:5]
 for w in late:
     print(f"  warp {w} (cta {w // 8}): start {(buf[w,0]-t0)/1e3:.2f} loop end {(buf[w,1]-t0)/1e3:.2f} stitch end {(buf[w,2]-t0)/1e3:.2f}")
+# what explains a warp's loop time: its boundaries, its warp slot, its CTA?
+n = A.shape[0]
+pos = np.unique(np.concatenate([np.minimum(Q[:, 0], Q[:, 1]), np.maximum(Q[:, 0], Q[:, 1])]).astype(np.int64))
+b0, blast = int(pos[0]), int(pos[-1])
+tiles = (n + 4095) // 4096
+G = (W // 8) if False else int(np.max(np.nonzero(buf[:, 0])[0]) // 8 + 1)
+R = (tiles + G - 1) // G
+cnts, times, slots = [], [], []
+for cta in range(G):
+    ta, tb = max(cta * R, b0 // 4096), min(cta * R + R - 1, blast // 4096)
+    if ta > tb:
+        continue
+    w0, w1 = max(ta * 4, b0 // 1024), min(tb * 4 + 3, blast // 1024)
+    per = (w1 - w0 + 8) // 8
+    for w in range(8):
+        wa = w0 + w * per
+        wb = min(wa + per - 1, w1)
+        if wa > wb or buf[cta * 8 + w, 0] == 0:
+            continue
+        c = np.searchsorted(pos, (wb + 1) * 1024) - np.searchsorted(pos, wa * 1024)
+        cnts.append(c)
+        times.append((buf[cta * 8 + w, 1] - buf[cta * 8 + w, 0]) / 1e3)
+        slots.append(w)
+cnts, times, slots = np.array(cnts), np.array(times), np.array(slots)
+m = times > 20
+print(f"pieces {m.sum()}: boundaries mean {cnts[m].mean():.1f} sd {cnts[m].std():.1f}; loop time sd {times[m].std():.2f} us; "
+      f"corr(boundaries, time) {np.corrcoef(cnts[m], times[m])[0, 1]:.3f}")
+print("mean loop time by warp slot:", " ".join(f"{w}:{times[m & (slots == w)].mean():.2f}" for w in range(8)))
