@@ -19,6 +19,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnroll = 4;  // 16-byte vectors per lane in flight
+constexpr int kKeysU = 8;   // A_Q keys pass: a k = 512 block (256 vectors) in one round trip
 
 // k % 128 == 0, A 16-byte aligned: full blocks [0, nfull) with vector loads;
 // the trailing partial block (blk == nfull < nblk) with lane-strided scalars.
@@ -348,28 +349,39 @@ __global__ void __launch_bounds__(kThreads) k_block_argmin_keys_ml(
     uint64_t* __restrict__ b_dev) {
     brmq::pdl_wait();
     brmq::pdl_trigger();  // small grid: dependents may be scheduled now
-    const uint64_t len = len_dev ? *len_dev : len_max;
     const uint64_t blk = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
     const uint64_t lo = blk * k;
-    if (lo >= len) return;
     const unsigned lane = lane_id();
     const uint4* v4 = reinterpret_cast<const uint4*>(K + lo);
     const uint32_t nvec = k >> 1;  // multiple of 32
-    uint64_t best = kNoKey;
-    for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kUnroll) {
-        uint4 x[kUnroll];
+    // the first round's loads go out before the true length (written by the
+    // contraction) is read: within the allocation (len_max, padded to an even
+    // count) they are harmless, and the length masks them below -- one dependent
+    // round trip fewer per block
+    uint4 x[kKeysU];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t e = lo + 2 * uint64_t(v0 + 32 * u + lane);
-            x[u] = v0 + 32 * u < nvec && e < len ? ld_stream_u4(v4 + v0 + 32 * u + lane)
-                                                 : make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (int u = 0; u < kKeysU; ++u) {
+        const uint64_t e = lo + 2 * uint64_t(32 * u + lane);
+        x[u] = 32u * u < nvec && e < len_max ? ld_stream_u4(v4 + 32 * u + lane) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+    const uint64_t len = len_dev ? *len_dev : len_max;
+    if (b_dev && blockIdx.x == 0 && threadIdx.x == 0) *b_dev = (len + k - 1) / k;
+    if (lo >= len) return;
+    uint64_t best = kNoKey;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * kKeysU) {
+        if (v0) {
+#pragma unroll
+            for (int u = 0; u < kKeysU; ++u) {
+                const uint64_t e = lo + 2 * uint64_t(v0 + 32 * u + lane);
+                x[u] = v0 + 32 * u < nvec && e < len ? ld_stream_u4(v4 + v0 + 32 * u + lane)
+                                                     : make_uint4(~0u, ~0u, ~0u, ~0u);
+            }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < kKeysU; ++u) {
             if (v0 + 32 * u >= nvec) break;
             const uint64_t e = lo + 2 * uint64_t(v0 + 32 * u + lane);
-            uint64_t kk = (uint64_t(x[u].y) << 32) | x[u].x;
+            uint64_t kk = e < len ? (uint64_t(x[u].y) << 32) | x[u].x : kNoKey;
             if (e + 1 < len) kk = kmin(kk, (uint64_t(x[u].w) << 32) | x[u].z);
             kk = group_min_key<16>(kk);  // the half warp's sub-block
             if ((lane & 15u) == 0 && e < len) sub[e >> 5] = kk;
