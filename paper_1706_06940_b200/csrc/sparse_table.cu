@@ -29,19 +29,37 @@ __global__ void __launch_bounds__(NT) k_st_tile(uint64_t* __restrict__ ST, uint6
     brmq::pdl_wait();
     brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     extern __shared__ uint64_t smem[];
-    const uint64_t b = b_dev ? *b_dev : b_max;
     const uint64_t s = 1ull << base;
     const uint32_t W = T + (1u << D) - 1;
     const uint32_t g = blockIdx.x % groups;  // residue group
     const uint32_t tt = blockIdx.x / groups;  // t tile
     const uint64_t r0 = uint64_t(g) * R;
     const uint64_t t0 = uint64_t(tt) * T;
-    if (b < s || r0 + s * t0 + s > b) return;  // no valid level-`base` cell in this tile
     uint64_t* cur = smem;
     uint64_t* nxt = smem + size_t(W) * R;
     const uint64_t* row_in = ST + uint64_t(base) * b_max;
+    // The window's first kPV cells per thread are loaded before the true block
+    // count (written by the block-keys kernel) is read: within the table's
+    // allocation (b_max) they are harmless and the count masks them -- one
+    // dependent round trip fewer
+    constexpr int kPV = 4;
+    uint64_t pv[kPV];
+#pragma unroll
+    for (int u = 0; u < kPV; ++u) {
+        const uint32_t i = threadIdx.x + uint32_t(u) * NT;
+        const uint64_t c = r0 + i % R + ((t0 + i / R) << base);
+        pv[u] = i < W * R && c + s <= b_max ? row_in[c] : kNoKey;
+    }
+    const uint64_t b = b_dev ? *b_dev : b_max;
+    if (b < s || r0 + s * t0 + s > b) return;  // no valid level-`base` cell in this tile
     // level-`base` cell (r, t) is valid iff r + s*t <= b - s  <=>  t <= (b - s - r) >> base
-    for (uint32_t i = threadIdx.x; i < W * R; i += NT) {
+#pragma unroll
+    for (int u = 0; u < kPV; ++u) {
+        const uint32_t i = threadIdx.x + uint32_t(u) * NT;
+        const uint64_t c = r0 + i % R + ((t0 + i / R) << base);
+        if (i < W * R) cur[i] = c + s <= b ? pv[u] : kNoKey;
+    }
+    for (uint32_t i = threadIdx.x + kPV * NT; i < W * R; i += NT) {
         const uint32_t rl = i % R, tl = i / R;
         const uint64_t c = r0 + rl + ((t0 + tl) << base);
         cur[i] = c + s <= b ? row_in[c] : kNoKey;
