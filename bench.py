@@ -485,8 +485,9 @@ def run_ours(args) -> dict:
                        "gbs": pre_bytes / (pre_ms * 1e-3) / 1e9 if pre_ms > 0 else None,
                        "frac": pre_bytes / (pre_ms * 1e-3) / 1e9 / pk["hbm_gbs"] if pre_ms > 0 else None,
                        "query_ms": phases.get("query", (float("nan"),))[0],
-                       "method": "timing level 3: CUDA events (graph nodes) before the first kernel and "
-                                 "before the query kernel; every kernel of the solve up to the query"},
+                       "method": "timing level 3: a CUDA event on the stream before the solve's graph launch "
+                                 "and an event node before the query kernel; every kernel of the solve up to "
+                                 "the query (query_ms: event nodes around the query kernel)"},
         "stages_ms": {k: round(v[0], 5) for k, v in breakdown.items()},
         "dominant_stage": dom,
         "variants_queries_per_s": variants,

@@ -253,8 +253,18 @@ struct Timer {
     // timing level 3: two phases, "preprocess" (everything before the query kernel)
     // and "query" -- four event nodes per solve instead of two per stage
     bool ph_open = false;
+    // device solves: the "preprocess" phase opens with a plain event recorded on
+    // the stream before the graph launch (one event node fewer inside the graph;
+    // the window then starts where the bench's own window does)
+    void pre_launch(bool dev) {
+        if (c->timing != 3 || !dev || n >= BRMQ_MAX_STAGES) return;
+        cudaEventRecord(c->ev[2 * n], c->stream);
+        c->stage_names.emplace_back("preprocess");
+        c->stage_launches.push_back(0);
+        ph_open = true;
+    }
     void phase_begin(const char* name) {
-        if (c->timing != 3 || n >= BRMQ_MAX_STAGES) return;
+        if (c->timing != 3 || n >= BRMQ_MAX_STAGES || ph_open) return;
         record(c->ev[2 * n]);
         c->stage_names.emplace_back(name);
         c->stage_launches.push_back(0);
@@ -855,6 +865,7 @@ int brmq_solve_bbst(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_query*
     };
     const GraphKey key{0, A, n, Q, q, k, c->count_scans ? 1 : 0, answers, s};
     if (int rc = prepare_ctl(c, ctl)) return rc;
+    tm.pre_launch(dev);
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     return end_solve(c, dev, tm, [c, b, L, launches]() {
@@ -1251,6 +1262,7 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     };
     const GraphKey key{1, A, n, Q, q, k, sort_kind, answers, s};
     if (int rc = prepare_ctl(c, ctl)) return rc;
+    tm.pre_launch(dev);
     if (int rc = run_solve(c, key, dev, tm, launches, enqueue)) return rc;
     c->ctl_clean = true;  // the final kernel published and re-zeroed the header
     c->epoch_host += n_epochs;
