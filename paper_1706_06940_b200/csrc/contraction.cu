@@ -66,7 +66,7 @@ static_assert(kTile == (1 << kContractTileLog2), "partition tile size");
 #ifndef BRMQ_CONTRACT_MINB
 #define BRMQ_CONTRACT_MINB 2  // 2 CTAs per SM: <= 128 registers (129 would halve the residency)
 #endif
-constexpr int kDense = BRMQ_KDENSE;
+constexpr int kDense = BRMQ_KDENSE;  // flagged rows per warp tile above which rows close per lane
 #ifdef BRMQ_CONTRACT_STAMPS
 // A/B diagnostics: per warp (start, loop end, stitch end) %globaltimer stamps of the
 // last contraction launch (tools/contract_tail.py)
@@ -76,23 +76,23 @@ __device__ __forceinline__ unsigned long long cgt() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#endif  // flagged rows per warp tile above which rows close per lane
+#endif
 constexpr int kDenseEndpoints = 8;  // endpoints per warp tile from which only dense rows are compiled in
 
 // Rows of the current warp tile in the warp's swizzled shared rows (16-byte
 // chunk c of row r at byte r*128 + ((c ^ (r & 7)) << 4)), read with explicit
 // shared loads.
 struct Rows {
-    uint32_t stage;  // shared address of the warp's rows
-    uint64_t tile_lo;
+    uint32_t stage;    // shared address of the warp's rows
+    uint32_t tile_lo;  // (positions fit 32 bits; those past n are masked)
     __device__ __forceinline__ int4 chunk(uint32_t r, int c) const {
         return lds128(stage + r * 128u + ((uint32_t(c) ^ (r & 7u)) << 4));
     }
     __device__ __forceinline__ int32_t elem(uint32_t r, int j) const {
         return lds32(stage + elem_offset(r, j));
     }
-    __device__ __forceinline__ uint64_t pos(uint32_t r, int j) const {
-        return tile_lo + uint64_t(r) * kRow + j;
+    __device__ __forceinline__ uint32_t pos(uint32_t r, int j) const {
+        return tile_lo + r * uint32_t(kRow) + uint32_t(j);
     }
     static __device__ __forceinline__ uint32_t elem_offset(uint32_t r, int j) {
         return r * 128u + (((uint32_t(j) >> 2) ^ (r & 7u)) << 4) + ((j & 3) << 2);
@@ -449,14 +449,21 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     // lane r reads row r (128 B; chunk c at c ^ (r & 7): conflict-free both ways).
     int4 y[8];
     uint32_t fy = 0;  // bitmap word of the lane's row, one tile ahead
-    auto fetch = [&](uint64_t i) {
-        const uint64_t tile_lo = (wa + i) * kWTile;
-        if (VEC && tile_lo + kWTile <= c.n) {
-            const int4* A4 = reinterpret_cast<const int4*>(c.A + tile_lo);
+    // per-tile index arithmetic in 32 bits (warp tiles < 2^22): the loop's 64-bit
+    // tile / interior / tail tests were ~8% of the kernel's instructions at c2
+    const uint32_t wa32 = uint32_t(wa), cnt32 = uint32_t(cnt);
+    const uint32_t full_tiles = uint32_t(c.n / kWTile);  // warp tiles entirely inside A
+    const int4* A4base = reinterpret_cast<const int4*>(c.A) + lane;
+    const uint32_t* Bbase = c.bitmap + lane;
+    auto fetch = [&](uint32_t i) {
+        const uint32_t t = wa32 + i;
+        if (VEC && t < full_tiles) {
+            const int4* A4 = A4base + size_t(t) * (kWTile / 4);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(A4 + u * 32 + lane);
+            for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(A4 + u * 32);
 
-        } else {  // array tail / unaligned A: scalar loads, positions >= n read as 0 (masked later)
+        } else {
+            const uint64_t tile_lo = uint64_t(t) * kWTile;  // array tail / unaligned A: scalar loads, positions >= n read as 0 (masked later)
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const uint64_t p = tile_lo + 128u * u + 4u * lane;
@@ -466,7 +473,7 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
                 y[u].w = p + 3 < c.n ? __ldg(c.A + p + 3) : 0;
             }
         }
-        fy = c.bitmap[(wa + i) * 32 + lane];
+        fy = Bbase[size_t(t) * 32];
     };
     auto stage = [&]() {
 #pragma unroll
@@ -484,7 +491,7 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         }
         if (MARKED) __syncwarp();
     };
-    if (cnt) fetch(0);
+    if (cnt32) fetch(0);
     // A PDL secondary of the piece count (BbST_CON) waits here: the span, the epoch
     // and the bitmap come from the endpoint kernel before it (complete when this
     // grid was scheduled), so the first tile of A is already in flight; the
@@ -542,19 +549,18 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     SegMin carry{kNoKey, 0};  // open segment after the warp tiles done so far (warp-uniform)
     uint64_t head = kNoKey;   // lane-local until published
     bool head_set = false;
-    auto tile = [&](auto gen_tag, uint64_t i, uint32_t fl) {
+    auto tile = [&](auto gen_tag, uint32_t i, uint32_t fl) {
         constexpr bool GEN = decltype(gen_tag)::value;
-        const uint64_t t = wa + i;
-        const uint64_t tile_lo = t * kWTile;
-        const uint64_t p0 = tile_lo + uint64_t(lane) * kRow;
+        const uint32_t t = wa32 + i;
         int jlo = 0, jhi = kRow - 1;
         bool any = true;
-        if (GEN) {
+        if (GEN) {  // a tile crossing the span's ends (64-bit: positions past n may pass 2^32)
+            const uint64_t p0 = uint64_t(t) * kWTile + uint64_t(lane) * kRow;
             any = p0 <= blast && p0 + kRow - 1 >= b0;
             jlo = p0 >= b0 ? 0 : int(b0 - p0);
             jhi = p0 + kRow - 1 <= blast ? kRow - 1 : int(int64_t(blast) - int64_t(p0));
         }
-        const Rows rs{smem_u32(s_rows[warp]), tile_lo};
+        const Rows rs{smem_u32(s_rows[warp]), t * uint32_t(kWTile)};
         const unsigned fm = __ballot_sync(kFull, fl != 0);
 
         if (fm == 0) {  // no boundary in the warp tile: one leftmost minimum
@@ -721,7 +727,7 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
             }
         }
         if (fl) {  // consumed bitmap word: (rank prefix, bits) for the remap, then clear
-            const uint64_t w = t * 32 + lane;
+            const size_t w = size_t(t) * 32 + lane;
             if (c.word_info) c.word_info[w] = make_uint2(uint32_t(my_rank), fl);
             c.bitmap[w] = 0;
         }
@@ -738,16 +744,18 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     const uint64_t gw_dbg = uint64_t(blockIdx.x) * NW + warp;
     if (lane == 0) g_cstamp[gw_dbg][0] = cgt();
 #endif
-    if (cnt) stage();
-    for (uint64_t i = 0; i < cnt; ++i) {
+    // tiles [i_in0, i_in1) of the piece lie entirely inside the span
+    const uint32_t t_in0 = uint32_t((uint64_t(b0) + kWTile - 1) / kWTile), t_in1 = uint32_t((uint64_t(blast) + 1) / kWTile);
+    const uint32_t i_in0 = t_in0 > wa32 ? t_in0 - wa32 : 0u;
+    const uint32_t i_in1 = t_in1 > wa32 ? t_in1 - wa32 : 0u;
+    if (cnt32) stage();
+    for (uint32_t i = 0; i < cnt32; ++i) {
         const uint32_t fl = fy;
-        if (i + 1 < cnt) fetch(i + 1);  // in flight while tile i is reduced
-        const uint64_t tile_lo = (wa + i) * kWTile;
-        const bool interior = tile_lo >= b0 && tile_lo + kWTile - 1 <= blast;
-        if (interior) tile(std::false_type{}, i, fl);
+        if (i + 1 < cnt32) fetch(i + 1);  // in flight while tile i is reduced
+        if (i >= i_in0 && i < i_in1) tile(std::false_type{}, i, fl);
         else tile(std::true_type{}, i, fl);
         __syncwarp();
-        if (i + 1 < cnt) stage();
+        if (i + 1 < cnt32) stage();
     }
 
 #ifdef BRMQ_CONTRACT_STAMPS
