@@ -838,21 +838,22 @@ template <bool DIRECT>
 __device__ __forceinline__ uint64_t side_flat(const uint64_t* __restrict__ sub, bool act, uint32_t lo,
                                               uint32_t hi, uint32_t plo, uint32_t phi, uint32_t ks,
                                               RowTask& rl, RowTask& rr) {
-    const uint32_t sl = lo >> 5, sr = hi >> 5, sb = (sl >> ks) << ks, K = 1u << ks;
+    const uint32_t sl = lo >> 5, sr = hi >> 5, sb = (sl >> ks) << ks;
     const ulonglong2* sub2 = reinterpret_cast<const ulonglong2*>(sub + sb);
+    // interior sub-blocks (sl, sr) as a bit mask over the block's <= 16 offsets:
+    // one bit test per key (compile-time bit) instead of two range compares
+    const uint32_t dl = sl - sb, dr = sr - sb;
+    const uint32_t im = act ? (((1u << dr) - 1u) & ~((2u << dl) - 1u)) : 0u;
     ulonglong2 x[8];
 #pragma unroll
-    for (uint32_t c = 0; c < 8; ++c) {
-        const uint32_t s = sb + 2 * c;
-        x[c] = (act && 2 * c < K && s + 1 > sl && s < sr) ? __ldg(sub2 + c) : make_ulonglong2(kNoKey, kNoKey);
-    }
+    for (uint32_t c = 0; c < 8; ++c)
+        x[c] = (im >> (2 * c)) & 3u ? __ldg(sub2 + c) : make_ulonglong2(kNoKey, kNoKey);
     const uint64_t kl = act ? __ldg(sub + sl) : kNoKey, kr = act ? __ldg(sub + sr) : kNoKey;
     uint64_t cand = kNoKey;
 #pragma unroll
-    for (uint32_t c = 0; c < 8; ++c) {  // interior sub-blocks (sl, sr)
-        const uint32_t s = sb + 2 * c;
-        if (s > sl && s < sr) cand = kmin(cand, x[c].x);
-        if (s + 1 > sl && s + 1 < sr) cand = kmin(cand, x[c].y);
+    for (uint32_t c = 0; c < 8; ++c) {
+        if (im & (1u << (2 * c))) cand = kmin(cand, x[c].x);
+        if (im & (2u << (2 * c))) cand = kmin(cand, x[c].y);
     }
     rl.need = rr.need = false;
     if (act) {

@@ -18,6 +18,7 @@ BUDGET = {
     "k_query_flatINS0_6RowKeyENS0_15QueryContractedELi128": 32,
     "k_query_flatINS0_6RowKeyENS0_17QueryContractedWIELi128": 24,
     "k_query_flatINS0_6RowI32ILb1EEENS0_11QueryDirectELi128": 8,
+    "k_query_flatINS0_6RowI32ILb0EEENS0_11QueryDirectELi128": 8,  # unaligned A only
     "k_query_budgetINS0_7ElemKey": 8,
     "k_rs_pass": 16,
 }
