@@ -498,6 +498,7 @@ void brmq_ctx_destroy(brmq_ctx* c) {
 
 int brmq_ctx_set_stream(brmq_ctx* c, void* s) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // (an outstanding async solve belongs to the old settings)
     c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
     return BRMQ_OK;
 }
@@ -506,12 +507,14 @@ void* brmq_ctx_stream(brmq_ctx* c) { return c ? static_cast<void*>(c->stream) : 
 
 int brmq_ctx_set_timing(brmq_ctx* c, int enable) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // (an outstanding async solve belongs to the old settings)
     c->timing = enable < 0 ? 0 : (enable > 3 ? 1 : enable);
     return BRMQ_OK;
 }
 
 int brmq_ctx_set_counters(brmq_ctx* c, int enable) {
     if (!c) return fail(BRMQ_EINVAL, "null context");
+    if (int rc = settle_pending(c)) return rc;  // (an outstanding async solve belongs to the old settings)
     c->count_scans = enable != 0;
     return BRMQ_OK;
 }

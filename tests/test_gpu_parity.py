@@ -306,6 +306,14 @@ def test_async_device_solves(engine, orc):
             _solve_into(engine, "con_bitmap", dA, dQ, outs["con_bitmap"])
             engine.synchronize()
             assert np.array_equal(outs["con_bitmap"].cpu().numpy().view(np.uint64), want)
+            # switching the context's stream settles the outstanding solve first
+            outs["bbst"].fill_(-1)
+            torch.cuda.synchronize()
+            _solve_into(engine, "bbst", dA, dQ, outs["bbst"])
+            other = torch.cuda.Stream()
+            engine.set_stream(other.cuda_stream)
+            assert np.array_equal(outs["bbst"].cpu().numpy().view(np.uint64), want)
+            engine.set_stream(None)
     finally:
         engine.set_async(False)
 
