@@ -497,6 +497,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     // grid was scheduled), so the first tile of A is already in flight; the
     // per-piece / per-range counts below are the predecessor's (a no-op otherwise)
     brmq::pdl_wait();
+    // dependents may be scheduled now -- after the wait, so that everything before
+    // this grid is complete when they start (DESIGN 3.5: "two launches back")
+    brmq::pdl_trigger();
 
     // ---- rank bases: the CTA's from the endpoint stage's per-range counts, the
     // warp's from a popcount of its piece of the bitmap (loads overlap the ring)
@@ -812,7 +815,6 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
 
 template <bool VEC, bool MARKED, bool SPARSE = true, bool FUSE = false>
 __global__ void __launch_bounds__(NT, BRMQ_CONTRACT_MINB) k_contract(const __grid_constant__ ContractArgs c) {
-    brmq::pdl_trigger();  // small grid: dependents may be scheduled now
     contract_body<VEC, MARKED, SPARSE, FUSE>(c);  // (its griddepcontrol.wait follows the first loads)
 }
 
