@@ -71,6 +71,7 @@ constexpr int kDense = BRMQ_KDENSE;  // flagged rows per warp tile above which r
 // A/B diagnostics: per warp (start, loop end, stitch end) %globaltimer stamps of the
 // last contraction launch (tools/contract_tail.py)
 __device__ unsigned long long g_cstamp[kMaxContractRanges * 8][3];
+__device__ unsigned long long g_cstamp2[kMaxContractRanges * 8][3];  // (entry, rank bases known, wait released)
 __device__ __forceinline__ unsigned long long cgt() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -426,6 +427,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     __shared__ unsigned long long s_base;
     __shared__ uint32_t s_red[NW];
 
+#ifdef BRMQ_CONTRACT_STAMPS
+    if ((threadIdx.x & 31u) == 0) g_cstamp2[uint64_t(blockIdx.x) * NW + (threadIdx.x >> 5)][0] = cgt();
+#endif
     const uint32_t b0 = ~c.span[0], blast = c.span[1];
     if (b0 > blast) return;
     const uint32_t epoch = *c.epoch_dev + c.epoch_off;
@@ -500,6 +504,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
     // dependents may be scheduled now -- after the wait, so that everything before
     // this grid is complete when they start (DESIGN 3.5: "two launches back")
     brmq::pdl_trigger();
+#ifdef BRMQ_CONTRACT_STAMPS
+    if (lane == 0) g_cstamp2[cta * NW + warp][2] = cgt();
+#endif
 
     // ---- rank bases: the CTA's from the endpoint stage's per-range counts, the
     // warp's from a popcount of its piece of the bitmap (loads overlap the ring)
@@ -545,6 +552,9 @@ __device__ __forceinline__ void contract_body(const ContractArgs& c) {
         }
         __syncthreads();
     }
+#ifdef BRMQ_CONTRACT_STAMPS
+    if (lane == 0) g_cstamp2[cta * NW + warp][1] = cgt();
+#endif
     uint64_t rank_run = s_base;  // global rank of the warp's next boundary
     for (uint32_t w = 0; w < warp; ++w) rank_run += s_cnt[w];
     const uint64_t rank_first = rank_run;
@@ -856,6 +866,9 @@ extern "C" int brmq_debug_contract_stamps(unsigned long long* out, int n) {
     static unsigned long long zero[kMaxContractRanges * 8][3];
     cudaMemcpyToSymbol(g_cstamp, zero, sizeof(zero));
     return rc;
+}
+extern "C" int brmq_debug_contract_stamps2(unsigned long long* out, int n) {
+    return int(cudaMemcpyFromSymbol(out, g_cstamp2, size_t(n) * 3 * 8));
 }
 #endif
 

@@ -30,6 +30,9 @@ for it in range(4):
     eng.solve_batch_bbst_con(dA, dQ, 512, VARIANT_SORT[a.variant])
     torch.cuda.synchronize()
     f(buf.ctypes.data, W)
+    if hasattr(L, 'brmq_debug_contract_stamps2'):
+        buf2 = np.zeros((W, 3), np.uint64)
+        L.brmq_debug_contract_stamps2(C.c_void_p(buf2.ctypes.data), C.c_int(W))
 live = buf[(buf[:, 0] > 0) & (buf[:, 1] > 0)]
 t0 = live[:, 0].min()
 s, e1, e2 = (live[:, 0] - t0) / 1e3, (live[:, 1] - t0) / 1e3, (live[:, 2] - t0) / 1e3
@@ -55,6 +58,17 @@ print(f"CTAs {len(cta_max)}: within-CTA spread (max-min) mean {np.mean(cta_max -
 # SM pairing: CTAs b and b + 148 likely share an SM? print correlation of neighbours
 st_minus_loop = (live[:, 2] - live[:, 1]) / 1e3
 print(f"stitch time per warp: p50 {np.median(st_minus_loop):.2f} p90 {np.percentile(st_minus_loop, 90):.2f} max {st_minus_loop.max():.2f}")
+if 'buf2' in dir():
+    ok = (buf2[:, 0] > 0) & (buf[:, 0] > 0)
+    e0 = buf2[ok, 0].astype(np.int64); t00 = e0.min()
+    ent, bas, lps = (e0 - t00) / 1e3, (buf2[ok, 1].astype(np.int64) - t00) / 1e3, (buf[ok, 0].astype(np.int64) - t00) / 1e3
+    ends_all = (buf[ok, 2].astype(np.int64) - t00) / 1e3
+    print(f"from the first warp's entry: entry p50 {np.median(ent):.2f} max {ent.max():.2f}; rank bases known "
+          f"p10 {np.percentile(bas, 10):.2f} p50 {np.median(bas):.2f} p90 {np.percentile(bas, 90):.2f} max {bas.max():.2f}; "
+          f"loop start p50 {np.median(lps):.2f} max {lps.max():.2f}; kernel end {ends_all.max():.2f}")
+    wr = (buf2[ok, 2].astype(np.int64) - t00) / 1e3
+    print(f"wait released p10 {np.percentile(wr, 10):.2f} p50 {np.median(wr):.2f} max {wr.max():.2f}; "
+          f"bases - release p10 {np.percentile(bas - wr, 10):.2f} p50 {np.median(bas - wr):.2f} max {(bas - wr).max():.2f}")
 late = np.argsort(-(buf[:, 2].astype(np.int64) - int(t0)))[:5]
 for w in late:
     print(f"  warp {w} (cta {w // 8}): start {(buf[w,0]-t0)/1e3:.2f} loop end {(buf[w,1]-t0)/1e3:.2f} stitch end {(buf[w,2]-t0)/1e3:.2f}")
