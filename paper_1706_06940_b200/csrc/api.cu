@@ -1080,13 +1080,20 @@ int brmq_solve_bbst_con(brmq_ctx* c, const int32_t* A, uint64_t n, const brmq_qu
     if (n == 0) return fail(BRMQ_ERANGE, "query exceeds array bounds");
     CUDA_TRY(cudaSetDevice(c->device));
     const bool dev = is_device(flags);
-    const bool use_bitmap = sort_kind == 2;
     const uint64_t m = 2 * q;
+    const int bits = bits_for(n);
+    // the bitmap sort marks endpoints directly, unless the bitmap outgrows the L2
+    // and is dense enough to need several slice passes over the queries (c5-con:
+    // four): then the endpoints are bucketed once by their top bits and each
+    // bucket marked from shared memory (the MSD pipeline's marking, same bitmap)
+    int D_ = 0, Lb_ = 0;
+    const bool use_bitmap =
+        sort_kind == 2 && !(c->use_msd && brmq::collect_mark_slices(n, q) > 1 &&
+                            brmq::radix_partition_shape(bits, m, brmq::contract_bitmap_words(n), &D_, &Lb_));
     const uint64_t aq_max = m - 1;                       // |A_Q| <= 2q - 1
     const uint64_t b_max = (aq_max + k - 1) / k;
     const uint32_t L = brmq::floor_log2_u64(b_max) + 1;
     const uint64_t ntiles = brmq::contract_tiles(n);
-    const int bits = bits_for(n);
     uint32_t G = 0, R = 0;
     brmq::contract_partition(n, &G, &R);
     if (int rc = ensure_bitmap(c, n)) return rc;

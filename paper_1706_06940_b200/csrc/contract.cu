@@ -502,6 +502,12 @@ inline unsigned g256(uint64_t x) { return unsigned((x + 255) / 256); }
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+uint32_t collect_mark_slices(uint64_t n, uint64_t q) {
+    const uint64_t bm_bytes = 2 * q >= n / 256 ? n / 8 : 0;
+    constexpr uint64_t kSliceBytes = uint64_t(32) << 20;
+    return uint32_t((bm_bytes + kSliceBytes - 1) / kSliceBytes);
+}
+
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump, uint32_t epoch_by, uint64_t* fill0, uint64_t fill0_n,
@@ -519,9 +525,7 @@ int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, ui
     // L2 instead of missing to HBM: c5's 2e7 endpoints 0.47 -> 0.26 ms (64 MiB
     // slices: 0.28, 16 MiB: 0.34); c4's 2e6 would pay more for the extra passes
     // (0.10 -> 0.15 ms)
-    const uint64_t bm_bytes = bitmap && 2 * q >= n / 256 ? n / 8 : 0;
-    constexpr uint64_t kSliceBytes = uint64_t(32) << 20;
-    const uint32_t slices = uint32_t((bm_bytes + kSliceBytes - 1) / kSliceBytes);
+    const uint32_t slices = bitmap ? collect_mark_slices(n, q) : 0u;
     if (slices <= 1) {
         brmq::launch_k(k_collect, dim3(grid), dim3(kThreads), 0, s, reinterpret_cast<const ulonglong2*>(Q), q, n, keys, vals,
                                                bitmap, span, err, epoch_bump, epoch_by, 0u, ~0u,

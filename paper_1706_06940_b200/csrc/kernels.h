@@ -172,6 +172,9 @@ constexpr int kContractTileLog2 = 12;  // 4096-position tiles
 void contract_partition(uint64_t n, uint32_t* G, uint32_t* R);
 // fill0 / fill1 (nullable): ranges set to kNoKey on the way (ContractFuse's sub
 // and table row 0)
+// passes of k_collect's direct marking: 1, or one per 32 MiB slice of a bitmap
+// larger than the L2 hit by at least one endpoint per 8 words
+uint32_t collect_mark_slices(uint64_t n, uint64_t q);
 int launch_collect(const uint64_t* Q, uint64_t q, uint64_t n, uint32_t* keys, uint32_t* vals,
                    uint32_t* bitmap, uint32_t* span, uint32_t* err, cudaStream_t s,
                    uint32_t* epoch_bump = nullptr, uint32_t epoch_by = 0,

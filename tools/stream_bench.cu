@@ -205,6 +205,58 @@ __global__ void k_ldg8_sts(const int4* __restrict__ a, uint64_t nvec, unsigned* 
     if (lane == 0 && m == 0x12345678) atomicAdd(out, 1u);
 }
 
+// persistent 4 KB warp tiles with the contraction's transpose and one tile of
+// prefetch; the tiles a warp takes: CH = 0 one contiguous piece per warp (the
+// contraction today), else chunks of CH consecutive tiles dealt round-robin over
+// the warps (the grid sweeps A front to back, the tail is balanced to one chunk)
+template <int CH>
+__global__ void k_ldg8p_sts(const int4* __restrict__ a, uint64_t nvec, unsigned* out) {
+    __shared__ __align__(128) int4 sx[8][256];
+    const uint32_t nw = gridDim.x * blockDim.x / 32;
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tiles = uint32_t(nvec / 256);
+    auto tile_at = [&](uint32_t i) -> uint32_t {  // i-th tile of this warp, or ~0u
+        if (CH == 0) {
+            const uint32_t per = (tiles + nw - 1) / nw, t = w * per + i;
+            return i < per && t < tiles ? t : ~0u;
+        }
+        constexpr uint32_t C = CH ? CH : 1;
+        const uint32_t t = ((i / C) * nw + w) * C + i % C;
+        return t < tiles ? t : ~0u;
+    };
+    int m = 0x7FFFFFFF;
+    int4 y[8];
+    uint32_t t = tile_at(0);
+    if (t != ~0u)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(a + uint64_t(t) * 256 + u * 32 + lane);
+    for (uint32_t i = 0; t != ~0u; ++i) {
+        int4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = y[u];
+        t = tile_at(i + 1);
+        if (t != ~0u)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y[u] = ld_stream_v4(a + uint64_t(t) * 256 + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t row = 4u * u + (lane >> 3), ch = lane & 7u;
+            sx[warp][row * 8u + (ch ^ (row & 7u))] = x[u];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int4 v = sx[warp][lane * 8u + (c ^ (lane & 7u))];
+            m = __vimin3_s32(m, v.x, v.y);
+            m = __vimin3_s32(m, v.z, v.w);
+        }
+        __syncwarp();
+    }
+    m = __reduce_min_sync(0xffffffffu, m);
+    if (lane == 0 && m == 0x12345678) atomicAdd(out, 1u);
+}
+
 // persistent: CTA c streams contiguous range of tiles; S stages of T bytes.
 template <bool TMA2D>
 __global__ void k_ring(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ a,
@@ -316,6 +368,17 @@ int main(int argc, char** argv) {
                 reinterpret_cast<int4*>(a), nvec, out);
         });
     }
+    auto p8 = [&](auto kern, const char* nm) {
+        for (int per : {2, 3})
+            timeit((std::string(nm) + " cta/sm=" + std::to_string(per)).c_str(),
+                   [&] { kern<<<sms * per, 256>>>(reinterpret_cast<int4*>(a), nvec, out); });
+    };
+    p8(k_ldg8p_sts<0>, "p8 contiguous");
+    p8(k_ldg8p_sts<1>, "p8 chunk=1");
+    p8(k_ldg8p_sts<2>, "p8 chunk=2");
+    p8(k_ldg8p_sts<4>, "p8 chunk=4");
+    p8(k_ldg8p_sts<8>, "p8 chunk=8");
+    if (argc > 3) return 0;
     auto cpa = [&](auto kern, int S, int cpsm) {
         const size_t smem = size_t(8) * S * 2048;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
